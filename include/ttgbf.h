@@ -1,0 +1,237 @@
+/* ttgbf.h -- C-ABI of the B200-native TT grid-based filter (TT-GBF) hot path.
+ *
+ * Drop-in boundary for the reference's Python filter API
+ * (ttpmf.filters / ttpmf.tensor_train / ttpmf.tt_algorithms).  Every entry
+ * point takes plain pointers and sizes (device pointers unless stated) plus
+ * a cudaStream_t passed as void*, launches hand-written sm_100a kernels and
+ * returns a status code (0 = ok, see TTGBF_E_*).  No torch types appear here.
+ *
+ * Reference interface each entry point replaces (file:line in the reference
+ * package pkg/src/ttpmf):
+ *   ttgbf_filter_prior        filters.initial_pmd_tt            filters.py:497-513
+ *   ttgbf_filter_measure      filters.measurement_update (TT)   filters.py:521-563
+ *                             + filters.moments_from_pmd (TT)   filters.py:287-333
+ *   ttgbf_filter_time_update  filters.tt_fft_pmf_step, lines after the moments:
+ *                             grid_redesign (interp+finalize)   filters.py:799-824
+ *                             kernel cross + tt_fft_convolve    filters.py:959-964
+ *                             realign cross + finalize          filters.py:965-985
+ *   ttgbf_tt_round            tensor_train.tt_round             tensor_train.py:327-360
+ *   ttgbf_tt_hadamard         tensor_train.tt_hadamard          tensor_train.py:252-266
+ *   ttgbf_tt_fft_convolve     tt_algorithms.tt_fft_convolve     tt_algorithms.py:642-666
+ *   ttgbf_tt_interpolate      tt_algorithms.tt_interpolate      tt_algorithms.py:701-718
+ *   ttgbf_tt_eval_many        tensor_train.tt_eval_many         tensor_train.py:129-158
+ *   ttgbf_tt_eval_at_points   tt_algorithms.tt_eval_at_points   tt_algorithms.py:721-745
+ *   ttgbf_tt_sum_moments      tensor_train.tt_sum / tt_dot with rank-one coordinate
+ *                             TTs as used by moments_from_pmd   tensor_train.py:269-288
+ *   ttgbf_greedy_cross        tt_algorithms.greedy_cross        tt_algorithms.py:463-596
+ *                             (on the prior / likelihood / kernel black boxes)
+ *   ttgbf_negative_mass       filters._negative_mass_tt         filters.py:427-436
+ */
+#ifndef TTGBF_H
+#define TTGBF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TTGBF_MAXD 16
+#define TTGBF_MAXB 16
+
+/* status codes */
+#define TTGBF_OK 0
+#define TTGBF_E_ARG 1          /* ValueError: shapes / configuration            */
+#define TTGBF_E_NONFINITE 2    /* ValueError: evaluator returned a non-finite   */
+#define TTGBF_E_DEGENERATE 3   /* DegenerateDensityError (filters.py:120)       */
+#define TTGBF_E_WORKSPACE 4    /* per-filter workspace too small                */
+#define TTGBF_E_CACHE 5        /* evaluator cache capacity exhausted            */
+#define TTGBF_E_CUDA 6         /* CUDA launch / runtime error                   */
+#define TTGBF_E_LINALG 7       /* numpy.linalg.LinAlgError (singular F)         */
+#define TTGBF_E_DENSE_GUARD 8  /* DenseGuardError                                */
+
+/* Equidistant axis: coordinate i = base + step * (i - off), evaluated with a
+ * separate multiply and add (no FMA) so it equals numpy's construction in
+ * grids.design_grid (off = (n-1)//2) and Grid.from_bounds (off = 0). */
+typedef struct {
+  double base;
+  double step;
+  int32_t off;
+  int32_t n;
+} ttgbf_axis;
+
+/* Packed tensor train: core k (r[k] x n[k] x r[k+1], C order) starts at
+ * data + off[k] (doubles). */
+typedef struct {
+  int32_t d;
+  int32_t n[TTGBF_MAXD];
+  int32_t r[TTGBF_MAXD + 1];
+  int32_t pad;
+  int64_t off[TTGBF_MAXD];
+} ttgbf_tt;
+
+/* CrossConfig (tt_algorithms.py:93-115).  rng_state = numpy PCG64 state of
+ * default_rng(rng_seed): {state_lo, state_hi, inc_lo, inc_hi, has_uint32,
+ * uinteger}.  cache_cap bounds the evaluator cache (entries). */
+typedef struct {
+  double tol;
+  int32_t max_rank;
+  int32_t max_sweeps;
+  int32_t validation_count;
+  int32_t pad;
+  uint64_t rng_state[6];
+  int64_t cache_cap;
+} ttgbf_cross_cfg;
+
+/* GridConfig rounding/normalisation policy (filters.py:129-161); a
+ * round_max_rank <= 0 means None. */
+typedef struct {
+  double round_tol;
+  int32_t round_max_rank;
+  int32_t normalize_before_round;
+  int64_t densify_guard;
+} ttgbf_grid_cfg;
+
+typedef struct {
+  double achieved;
+  int64_t calls;
+  int32_t sweeps;
+  int32_t converged;
+} ttgbf_cross_info;
+
+#define TTGBF_NMOM (1 + TTGBF_MAXD + TTGBF_MAXD * (TTGBF_MAXD + 1) / 2)
+
+/* per-filter diagnostics (StepDiagnostics, filters.py:164-188) */
+typedef struct {
+  int32_t status;
+  int32_t outlier;
+  double mass_before_norm;
+  double clipped_mass;
+  ttgbf_cross_info cross[3];     /* prior|likelihood, kernel, realign */
+  double raw_moments[TTGBF_NMOM];/* sum, first (d), second (i<=j), un-normalised */
+  int64_t ws_peak;               /* bytes of workspace used */
+} ttgbf_diag;
+
+/* Model constants (StateSpaceModel, models.py:85-153).  Matrices row-major
+ * with leading dimension TTGBF_MAXD (F, Finv, Lq, H) or TTGBF_MAXB (Lr).
+ * Lq / Lr are numpy's lower Cholesky factors of Q / R; logn_* the
+ * GaussianDensity log normalisers (models.py:47-49). */
+typedef struct {
+  int32_t d;
+  int32_t b;
+  int32_t hkind;      /* 0 linear, 1 range_bearing, 2 range_bearing_deg,
+                         3 norm_bearing_deg, 4 abs_first, 5 range_az_el,
+                         6 chain_quadratic */
+  int32_t nang;
+  int32_t ang[TTGBF_MAXB];
+  double F[TTGBF_MAXD * TTGBF_MAXD];
+  double Finv[TTGBF_MAXD * TTGBF_MAXD];
+  double Lq[TTGBF_MAXD * TTGBF_MAXD];
+  double logn_q;
+  double Lr[TTGBF_MAXB * TTGBF_MAXB];
+  double logn_r;
+  double H[TTGBF_MAXB * TTGBF_MAXD];
+} ttgbf_model;
+
+/* Gaussian prior (initial_pmd_tt) */
+typedef struct {
+  double mean[TTGBF_MAXD];
+  double L[TTGBF_MAXD * TTGBF_MAXD];
+  double logn;
+} ttgbf_gauss;
+
+/* per-filter step inputs: current grid, pre-convolution (filtering) grid,
+ * predictive grid (from the host-side redesign), measurement */
+typedef struct {
+  ttgbf_axis cur[TTGBF_MAXD];
+  ttgbf_axis filt[TTGBF_MAXD];
+  ttgbf_axis pred[TTGBF_MAXD];
+  double z[TTGBF_MAXB];
+  int32_t has_z;
+  int32_t active;
+} ttgbf_filter_io;
+
+/* ---- filter stages: one CTA per filter, nfilt filters per launch ---------
+ * state_hdr[f] / state + f*state_cap: the filter's TT weights (in/out).
+ * ws + f*ws_bytes: per-filter workspace.  probes: negative-mass probe cells
+ * (nprobes x d, int32) of default_rng(0); seeds: _seed_lattice cells
+ * (nseeds x d) -- both depend only on the grid shape. */
+int ttgbf_filter_prior(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg,
+                       ttgbf_cross_cfg xcfg, const ttgbf_filter_io* io, int nfilt,
+                       const int32_t* probes, int nprobes, ttgbf_tt* state_hdr, double* state,
+                       int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag, void* stream);
+
+int ttgbf_filter_measure(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
+                         const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
+                         const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr, double* state,
+                         int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag, void* stream);
+
+int ttgbf_filter_time_update(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
+                             const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
+                             const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr, double* state,
+                             int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag,
+                             void* stream);
+
+/* ---- TT primitives (batched over `count` independent items, one CTA each).
+ * Inputs/outputs are arrays of packed TTs: hdr[i] with data + i*cap. ---- */
+int ttgbf_tt_round(const ttgbf_tt* in_hdr, const double* in, int64_t in_cap, int count, double tol,
+                   int max_rank, ttgbf_tt* out_hdr, double* out, int64_t out_cap, void* ws,
+                   int64_t ws_bytes, int32_t* status, void* stream);
+
+int ttgbf_tt_hadamard(const ttgbf_tt* a_hdr, const double* a, int64_t a_cap, const ttgbf_tt* b_hdr,
+                      const double* b, int64_t b_cap, int count, ttgbf_tt* out_hdr, double* out,
+                      int64_t out_cap, void* ws, int64_t ws_bytes, int32_t* status, void* stream);
+
+int ttgbf_tt_fft_convolve(const ttgbf_tt* k_hdr, const double* k, int64_t k_cap, const ttgbf_tt* w_hdr,
+                          const double* w, int64_t w_cap, int count, double tol, int max_rank,
+                          ttgbf_tt* out_hdr, double* out, int64_t out_cap, void* ws, int64_t ws_bytes,
+                          int32_t* status, void* stream);
+
+/* old/new axes: arrays of d ttgbf_axis per item (device) */
+int ttgbf_tt_interpolate(const ttgbf_tt* in_hdr, const double* in, int64_t in_cap, int count,
+                         const ttgbf_axis* old_axes, const ttgbf_axis* new_axes, ttgbf_tt* out_hdr,
+                         double* out, int64_t out_cap, void* ws, int64_t ws_bytes, int32_t* status,
+                         void* stream);
+
+/* idx: K x d int32 per item (item stride K*d); out: K per item */
+int ttgbf_tt_eval_many(const ttgbf_tt* hdr, const double* data, int64_t cap, int count, const int32_t* idx,
+                       int64_t K, double* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream);
+
+/* pts: K x d doubles per item; axes: d ttgbf_axis per item */
+int ttgbf_tt_eval_at_points(const ttgbf_tt* hdr, const double* data, int64_t cap, int count,
+                            const ttgbf_axis* axes, const double* pts, int64_t K, double* out, void* ws,
+                            int64_t ws_bytes, int32_t* status, void* stream);
+
+/* out per item: TTGBF_NMOM doubles (sum, first, second raw moments against
+ * the axis coordinates; axes: d ttgbf_axis per item) */
+int ttgbf_tt_sum_moments(const ttgbf_tt* hdr, const double* data, int64_t cap, int count,
+                         const ttgbf_axis* axes, double* out, void* ws, int64_t ws_bytes, int32_t* status,
+                         void* stream);
+
+/* black-box kinds for ttgbf_greedy_cross */
+#define TTGBF_BB_GAUSS 0       /* prior pdf on the grid (uses prior)           */
+#define TTGBF_BB_LIKELIHOOD 1  /* p(z|x) on the grid (uses model, io.z)        */
+#define TTGBF_BB_KERNEL 2      /* FFT kernel on the grid (uses model)          */
+
+int ttgbf_greedy_cross(int kind, const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_cross_cfg xcfg,
+                       const ttgbf_filter_io* io, int count, const int32_t* seeds, int nseeds,
+                       ttgbf_tt* out_hdr, double* out, int64_t out_cap, void* ws, int64_t ws_bytes,
+                       ttgbf_diag* diag, void* stream);
+
+/* negative mass of a normalised TT on grid `axes` (returned already
+ * multiplied by the cell volume) */
+int ttgbf_negative_mass(const ttgbf_tt* hdr, const double* data, int64_t cap, int count,
+                        const ttgbf_axis* axes, int64_t guard, const int32_t* probes, int nprobes,
+                        double* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream);
+
+/* library info */
+int ttgbf_version(void);
+int ttgbf_block_threads(void);
+int64_t ttgbf_smem_bytes(void);
+const char* ttgbf_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TTGBF_H */

@@ -1,0 +1,116 @@
+"""ctypes / numpy mirror of ``include/ttgbf.h`` and the product library loader.
+
+The product library is ``paper_2501_07942_b200/_lib/libttgbf.so`` (sm_100a,
+built in-tree by :func:`paper_2501_07942_b200.build.build`).  There is no CPU
+fallback: :func:`load_library` raises if the library or a CUDA device is
+missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+MAXD = 16
+MAXB = 16
+NMOM = 1 + MAXD + MAXD * (MAXD + 1) // 2
+
+STATUS = {
+    0: "ok", 1: "invalid argument / shape", 2: "evaluator returned a non-finite value",
+    3: "TT weights carry no probability mass", 4: "per-filter workspace exhausted",
+    5: "evaluator cache capacity exhausted", 6: "CUDA error", 7: "singular matrix",
+    8: "dense guard exceeded",
+}
+E_ARG, E_NONFINITE, E_DEGENERATE, E_WORKSPACE, E_CACHE = 1, 2, 3, 4, 5
+
+AXIS = np.dtype([("base", "f8"), ("step", "f8"), ("off", "i4"), ("n", "i4")], align=True)
+TT = np.dtype([("d", "i4"), ("n", "i4", MAXD), ("r", "i4", MAXD + 1), ("pad", "i4"),
+               ("off", "i8", MAXD)], align=True)
+CROSS_INFO = np.dtype([("achieved", "f8"), ("calls", "i8"), ("sweeps", "i4"), ("converged", "i4")],
+                      align=True)
+DIAG = np.dtype([("status", "i4"), ("outlier", "i4"), ("mass_before_norm", "f8"),
+                 ("clipped_mass", "f8"), ("cross", CROSS_INFO, 3), ("raw_moments", "f8", NMOM),
+                 ("ws_peak", "i8")], align=True)
+MODEL = np.dtype([("d", "i4"), ("b", "i4"), ("hkind", "i4"), ("nang", "i4"), ("ang", "i4", MAXB),
+                  ("F", "f8", MAXD * MAXD), ("Finv", "f8", MAXD * MAXD), ("Lq", "f8", MAXD * MAXD),
+                  ("logn_q", "f8"), ("Lr", "f8", MAXB * MAXB), ("logn_r", "f8"),
+                  ("H", "f8", MAXB * MAXD)], align=True)
+GAUSS = np.dtype([("mean", "f8", MAXD), ("L", "f8", MAXD * MAXD), ("logn", "f8")], align=True)
+FILTER_IO = np.dtype([("cur", AXIS, MAXD), ("filt", AXIS, MAXD), ("pred", AXIS, MAXD),
+                      ("z", "f8", MAXB), ("has_z", "i4"), ("active", "i4")], align=True)
+
+
+class GridCfg(ctypes.Structure):
+    _fields_ = [("round_tol", ctypes.c_double), ("round_max_rank", ctypes.c_int32),
+                ("normalize_before_round", ctypes.c_int32), ("densify_guard", ctypes.c_int64)]
+
+
+class CrossCfg(ctypes.Structure):
+    _fields_ = [("tol", ctypes.c_double), ("max_rank", ctypes.c_int32),
+                ("max_sweeps", ctypes.c_int32), ("validation_count", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("rng_state", ctypes.c_uint64 * 6),
+                ("cache_cap", ctypes.c_int64)]
+
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+F64 = ctypes.c_double
+
+SIGNATURES = {
+    "ttgbf_filter_prior": [P, P, GridCfg, CrossCfg, P, I32, P, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_filter_measure": [P, GridCfg, CrossCfg, P, I32, P, I32, P, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_filter_time_update": [P, GridCfg, CrossCfg, P, I32, P, I32, P, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_tt_round": [P, P, I64, I32, F64, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_tt_hadamard": [P, P, I64, P, P, I64, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_tt_fft_convolve": [P, P, I64, P, P, I64, I32, F64, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_tt_interpolate": [P, P, I64, I32, P, P, P, P, I64, P, I64, P, P],
+    "ttgbf_tt_eval_many": [P, P, I64, I32, P, I64, P, P, I64, P, P],
+    "ttgbf_tt_eval_at_points": [P, P, I64, I32, P, P, I64, P, P, I64, P, P],
+    "ttgbf_tt_sum_moments": [P, P, I64, I32, P, P, P, I64, P, P],
+    "ttgbf_greedy_cross": [I32, P, P, CrossCfg, P, I32, P, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_negative_mass": [P, P, I64, I32, P, I64, P, I32, P, P, I64, P, P],
+    "ttgbf_version": [],
+    "ttgbf_block_threads": [],
+    "ttgbf_smem_bytes": [],
+    "ttgbf_status_string": [I32],
+}
+RESTYPES = {"ttgbf_smem_bytes": I64, "ttgbf_status_string": ctypes.c_char_p}
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(HERE, "_lib")
+PRODUCT_LIB = os.path.join(LIB_DIR, "libttgbf.so")
+
+
+def bind(lib):
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = RESTYPES.get(name, I32)
+    return lib
+
+
+_LIB = None
+
+
+def load_library():
+    """Load the sm_100a product library; raise loudly if it cannot run here."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(PRODUCT_LIB):
+        raise RuntimeError(
+            f"{PRODUCT_LIB} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("the TT-GBF hot path needs a CUDA device (B200, sm_100a); none is visible")
+    torch.cuda.init()
+    _LIB = bind(ctypes.CDLL(PRODUCT_LIB))
+    return _LIB
+
+
+def status_text(code: int) -> str:
+    return STATUS.get(int(code), f"status {int(code)}")

@@ -1,0 +1,247 @@
+// C-ABI entry points (include/ttgbf.h).  Each entry point launches ONE
+// kernel with one 256-thread CTA per item (filter or TT) on the caller's
+// stream; per-item status codes land in device memory.
+//
+// Built by nvcc for sm_100a this is the product library libttgbf.so.
+// Built by g++ with -DENGINE_HOSTSIM (tests only) the same source becomes
+// libttgbf_hostsim.so, whose "launch" loops over items on the CPU with a
+// one-thread CTA; the product package never loads it.
+#include "bodies.cuh"
+
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#define LAMBDA [=] __device__
+#else
+#include <vector>
+#define LAMBDA [=]
+#endif
+
+using namespace tg;
+
+namespace {
+
+#ifdef __CUDACC__
+template <class F>
+__global__ void __launch_bounds__(BLOCK_THREADS) k_items(F f, int count) {
+  extern __shared__ double smem[];
+  const Ctx c = make_ctx(smem, threadIdx.x, blockDim.x);
+  if ((int)blockIdx.x < count) f(c, (int)blockIdx.x, smem);
+}
+
+template <class F>
+int launch(int count, F f, void* stream) {
+  if (count <= 0) return TTGBF_OK;
+  const size_t smem = (size_t)SMEM_DOUBLES * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(k_items<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return TTGBF_E_CUDA;
+  k_items<F><<<count, BLOCK_THREADS, smem, (cudaStream_t)stream>>>(f, count);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? TTGBF_OK : TTGBF_E_CUDA;
+}
+#else
+template <class F>
+int launch(int count, F f, void*) {
+  std::vector<double> smem(SMEM_DOUBLES);
+  for (int i = 0; i < count; ++i) {
+    const Ctx c = make_ctx(smem.data(), 0, 1);
+    f(c, i, smem.data());
+  }
+  return TTGBF_OK;
+}
+#endif
+
+}  // namespace
+
+extern "C" {
+
+int ttgbf_version(void) { return 1; }
+int ttgbf_block_threads(void) { return BLOCK_THREADS; }
+int64_t ttgbf_smem_bytes(void) { return (int64_t)SMEM_DOUBLES * 8; }
+
+const char* ttgbf_status_string(int s) {
+  switch (s) {
+    case TTGBF_OK: return "ok";
+    case TTGBF_E_ARG: return "invalid argument / shape";
+    case TTGBF_E_NONFINITE: return "evaluator returned a non-finite value";
+    case TTGBF_E_DEGENERATE: return "TT weights carry no probability mass";
+    case TTGBF_E_WORKSPACE: return "per-filter workspace exhausted";
+    case TTGBF_E_CACHE: return "evaluator cache capacity exhausted";
+    case TTGBF_E_CUDA: return "CUDA error";
+    case TTGBF_E_LINALG: return "singular matrix";
+    case TTGBF_E_DENSE_GUARD: return "dense guard exceeded";
+    default: return "unknown status";
+  }
+}
+
+// ---------------------------------------------------------------- stages
+int ttgbf_filter_prior(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg,
+                       ttgbf_cross_cfg xcfg, const ttgbf_filter_io* io, int nfilt, const int32_t* probes,
+                       int nprobes, ttgbf_tt* state_hdr, double* state, int64_t state_cap, void* ws,
+                       int64_t ws_bytes, ttgbf_diag* diag, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    if (!io[i].active) return;
+    Arena ar = make_arena(ws, ws_bytes, i);
+    ttgbf_diag* dg = diag + i;
+    if (c.leader()) { dg->clipped_mass = 0.0; dg->outlier = 0; }
+    c.sync();
+    int st = stage_prior(c, ar, *model, *prior, gcfg, xcfg, io[i], probes, nprobes, state_hdr + i,
+                         state + (int64_t)i * state_cap, state_cap, dg, make_stage_smem(smem));
+    if (c.leader()) { dg->status = st; dg->ws_peak = (int64_t)ar.peak; }
+  };
+  return launch(nfilt, f, stream);
+}
+
+int ttgbf_filter_measure(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
+                         const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
+                         const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr, double* state,
+                         int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    if (!io[i].active) return;
+    Arena ar = make_arena(ws, ws_bytes, i);
+    ttgbf_diag* dg = diag + i;
+    if (c.leader()) { dg->clipped_mass = 0.0; dg->outlier = 0; dg->mass_before_norm = NAN; }
+    c.sync();
+    int st = stage_measure(c, ar, *model, gcfg, xcfg, io[i], probes, nprobes, seeds, nseeds, state_hdr + i,
+                           state + (int64_t)i * state_cap, state_cap, dg, make_stage_smem(smem));
+    if (c.leader()) { dg->status = st; dg->ws_peak = (int64_t)ar.peak; }
+  };
+  return launch(nfilt, f, stream);
+}
+
+int ttgbf_filter_time_update(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
+                             const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
+                             const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr, double* state,
+                             int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    if (!io[i].active) return;
+    Arena ar = make_arena(ws, ws_bytes, i);
+    ttgbf_diag* dg = diag + i;
+    int st = stage_time(c, ar, *model, gcfg, xcfg, io[i], probes, nprobes, seeds, nseeds, state_hdr + i,
+                        state + (int64_t)i * state_cap, state_cap, dg, make_stage_smem(smem));
+    if (c.leader()) {
+      dg->status = st;
+      if ((int64_t)ar.peak > dg->ws_peak) dg->ws_peak = (int64_t)ar.peak;
+    }
+  };
+  return launch(nfilt, f, stream);
+}
+
+// ---------------------------------------------------------------- TT primitives
+int ttgbf_tt_round(const ttgbf_tt* in_hdr, const double* in, int64_t in_cap, int count, double tol, int max_rank,
+                   ttgbf_tt* out_hdr, double* out, int64_t out_cap, void* ws, int64_t ws_bytes, int32_t* status,
+                   void* stream) {
+  if (tol < 0.0) return TTGBF_E_ARG;
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    Arena ar = make_arena(ws, ws_bytes, i);
+    int st = body_round(c, ar, in_hdr + i, in + (int64_t)i * in_cap, tol, max_rank, out_hdr + i,
+                        out + (int64_t)i * out_cap, out_cap, make_stage_smem(smem).sm);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+int ttgbf_tt_hadamard(const ttgbf_tt* a_hdr, const double* a, int64_t a_cap, const ttgbf_tt* b_hdr, const double* b,
+                      int64_t b_cap, int count, ttgbf_tt* out_hdr, double* out, int64_t out_cap, void* ws,
+                      int64_t ws_bytes, int32_t* status, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    (void)smem;
+    Arena ar = make_arena(ws, ws_bytes, i);
+    int st = body_hadamard(c, ar, a_hdr + i, a + (int64_t)i * a_cap, b_hdr + i, b + (int64_t)i * b_cap,
+                           out_hdr + i, out + (int64_t)i * out_cap, out_cap);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+int ttgbf_tt_fft_convolve(const ttgbf_tt* k_hdr, const double* k, int64_t k_cap, const ttgbf_tt* w_hdr,
+                          const double* w, int64_t w_cap, int count, double tol, int max_rank, ttgbf_tt* out_hdr,
+                          double* out, int64_t out_cap, void* ws, int64_t ws_bytes, int32_t* status, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    Arena ar = make_arena(ws, ws_bytes, i);
+    int st = body_fftconv(c, ar, k_hdr + i, k + (int64_t)i * k_cap, w_hdr + i, w + (int64_t)i * w_cap, tol,
+                          max_rank, out_hdr + i, out + (int64_t)i * out_cap, out_cap, make_stage_smem(smem).sm);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+int ttgbf_tt_interpolate(const ttgbf_tt* in_hdr, const double* in, int64_t in_cap, int count,
+                         const ttgbf_axis* old_axes, const ttgbf_axis* new_axes, ttgbf_tt* out_hdr, double* out,
+                         int64_t out_cap, void* ws, int64_t ws_bytes, int32_t* status, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    (void)smem;
+    Arena ar = make_arena(ws, ws_bytes, i);
+    const int d = in_hdr[i].d;
+    int st = body_interp(c, ar, in_hdr + i, in + (int64_t)i * in_cap, old_axes + (int64_t)i * d,
+                         new_axes + (int64_t)i * d, out_hdr + i, out + (int64_t)i * out_cap, out_cap);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+int ttgbf_tt_eval_many(const ttgbf_tt* hdr, const double* data, int64_t cap, int count, const int32_t* idx, int64_t K,
+                       double* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    const int d = hdr[i].d;
+    int st = body_eval_many(c, hdr + i, data + (int64_t)i * cap, idx + (int64_t)i * K * d, K, out + (int64_t)i * K,
+                            make_stage_smem(smem).sm);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+int ttgbf_tt_eval_at_points(const ttgbf_tt* hdr, const double* data, int64_t cap, int count, const ttgbf_axis* axes,
+                            const double* pts, int64_t K, double* out, void* ws, int64_t ws_bytes, int32_t* status,
+                            void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    Arena ar = make_arena(ws, ws_bytes, i);
+    const int d = hdr[i].d;
+    int st = body_eval_points(c, ar, hdr + i, data + (int64_t)i * cap, axes + (int64_t)i * d,
+                              pts + (int64_t)i * K * d, K, out + (int64_t)i * K, make_stage_smem(smem).sm);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+int ttgbf_tt_sum_moments(const ttgbf_tt* hdr, const double* data, int64_t cap, int count, const ttgbf_axis* axes,
+                         double* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    (void)smem;
+    Arena ar = make_arena(ws, ws_bytes, i);
+    const int d = hdr[i].d;
+    int st = body_moments(c, ar, hdr + i, data + (int64_t)i * cap, axes + (int64_t)i * d,
+                          out + (int64_t)i * TTGBF_NMOM);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+int ttgbf_greedy_cross(int kind, const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_cross_cfg xcfg,
+                       const ttgbf_filter_io* io, int count, const int32_t* seeds, int nseeds, ttgbf_tt* out_hdr,
+                       double* out, int64_t out_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag, void* stream) {
+  if (kind < 0 || kind > 2) return TTGBF_E_ARG;
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    Arena ar = make_arena(ws, ws_bytes, i);
+    int st = body_cross(c, ar, kind, *model, prior, xcfg, io[i], seeds, nseeds, out_hdr + i,
+                        out + (int64_t)i * out_cap, out_cap, diag + i, make_stage_smem(smem));
+    if (c.leader()) { diag[i].status = st; diag[i].ws_peak = (int64_t)ar.peak; }
+  };
+  return launch(count, f, stream);
+}
+
+int ttgbf_negative_mass(const ttgbf_tt* hdr, const double* data, int64_t cap, int count, const ttgbf_axis* axes,
+                        int64_t guard, const int32_t* probes, int nprobes, double* out, void* ws, int64_t ws_bytes,
+                        int32_t* status, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    Arena ar = make_arena(ws, ws_bytes, i);
+    const int d = hdr[i].d;
+    int st = body_negmass(c, ar, hdr + i, data + (int64_t)i * cap, axes + (int64_t)i * d, guard, probes, nprobes,
+                          out + i, make_stage_smem(smem).sm);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+}  // extern "C"

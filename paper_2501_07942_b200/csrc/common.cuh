@@ -1,0 +1,225 @@
+// Common layer of the TT-GBF step engine.
+//
+// The engine is written as CTA-cooperative C++: every routine is executed by
+// all threads of one CTA with uniform control flow; parallel loops stride by
+// `nt`, serial sections run on thread 0 and publish through memory followed by
+// a barrier.  Compiled by nvcc this is the product (one CTA per filter,
+// sm_100a).  Compiled by g++ (ENGINE_HOSTSIM) the same source runs as a single
+// "thread" -- used only by the CPU test-suite to check the engine's decision
+// logic against the oracle; it is never loaded by the product path.
+#pragma once
+
+#include <stdint.h>
+#include <stddef.h>
+#include <math.h>
+#include <string.h>
+
+#ifdef __CUDACC__
+#define HD __host__ __device__ __forceinline__
+#define HDI __host__ __device__
+#define HDN __host__ __device__ __noinline__
+#else
+#define HD inline
+#define HDI
+#define HDN inline
+#endif
+
+#if defined(__CUDA_ARCH__)
+#define ENGINE_DEVICE 1
+#else
+#define ENGINE_DEVICE 0
+#endif
+
+namespace tg {
+
+constexpr int MAXD = 16;      // max number of modes (state dimension)
+constexpr int MAXB = 16;      // max measurement dimension
+
+// status codes (mirrored in include/ttgbf.h)
+enum Status : int {
+  OK = 0,
+  E_ARG = 1,          // ValueError: bad shape / config
+  E_NONFINITE = 2,    // ValueError: evaluator returned a non-finite value
+  E_DEGENERATE = 3,   // DegenerateDensityError
+  E_WORKSPACE = 4,    // per-filter workspace exhausted
+  E_CACHE = 5,        // evaluator cache capacity exhausted
+  E_CUDA = 6,
+  E_LINALG = 7,       // singular dynamics (numpy.linalg.LinAlgError)
+  E_DENSE_GUARD = 8,  // DenseGuardError
+};
+
+#define CK(expr) do { int _st = (expr); if (_st) return _st; } while (0)
+
+HD int imin(int a, int b) { return a < b ? a : b; }
+HD int imax(int a, int b) { return a > b ? a : b; }
+HD int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
+HD int64_t lmax(int64_t a, int64_t b) { return a > b ? a : b; }
+
+// ---------------------------------------------------------------------------
+// CTA context
+// ---------------------------------------------------------------------------
+struct Ctx {
+  int tid;
+  int nt;
+  double* red;   // shared scratch, >= 64 doubles (+ 64 ints after it)
+  int* ired;     // shared scratch, >= 64 ints
+
+  HD void sync() const {
+#if ENGINE_DEVICE
+    __syncthreads();
+#endif
+  }
+  HD bool leader() const { return tid == 0; }
+};
+
+// Deterministic CTA-wide sum: warp shuffles, then every thread adds the warp
+// partials in warp order.  All threads must call; all receive the result.
+HD double block_sum(const Ctx& c, double v) {
+#if ENGINE_DEVICE
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = c.tid >> 5, l = c.tid & 31, nw = (c.nt + 31) >> 5;
+  __syncthreads();
+  if (l == 0) c.red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += c.red[i];
+  __syncthreads();
+  return s;
+#else
+  (void)c;
+  return v;
+#endif
+}
+
+HD double block_max(const Ctx& c, double v) {
+#if ENGINE_DEVICE
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = c.tid >> 5, l = c.tid & 31, nw = (c.nt + 31) >> 5;
+  __syncthreads();
+  if (l == 0) c.red[w] = v;
+  __syncthreads();
+  double s = c.red[0];
+  for (int i = 1; i < nw; ++i) s = fmax(s, c.red[i]);
+  __syncthreads();
+  return s;
+#else
+  (void)c;
+  return v;
+#endif
+}
+
+HD int64_t block_sum_i64(const Ctx& c, int64_t v) {
+#if ENGINE_DEVICE
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = c.tid >> 5, l = c.tid & 31, nw = (c.nt + 31) >> 5;
+  int64_t* r = reinterpret_cast<int64_t*>(c.red);
+  __syncthreads();
+  if (l == 0) r[w] = v;
+  __syncthreads();
+  int64_t s = 0;
+  for (int i = 0; i < nw; ++i) s += r[i];
+  __syncthreads();
+  return s;
+#else
+  (void)c;
+  return v;
+#endif
+}
+
+// argmax with numpy semantics: largest value, first index among ties.
+struct ValIdx {
+  double v;
+  int64_t i;
+};
+HD ValIdx vi_better(ValIdx a, ValIdx b) {
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+HD ValIdx block_argmax(const Ctx& c, ValIdx x) {
+#if ENGINE_DEVICE
+  for (int o = 16; o > 0; o >>= 1) {
+    ValIdx y;
+    y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+    x = vi_better(x, y);
+  }
+  const int w = c.tid >> 5, l = c.tid & 31, nw = (c.nt + 31) >> 5;
+  int64_t* ri = reinterpret_cast<int64_t*>(c.red + 32);
+  __syncthreads();
+  if (l == 0) { c.red[w] = x.v; ri[w] = x.i; }
+  __syncthreads();
+  ValIdx s{c.red[0], ri[0]};
+  for (int i = 1; i < nw; ++i) s = vi_better(s, ValIdx{c.red[i], ri[i]});
+  __syncthreads();
+  return s;
+#else
+  (void)c;
+  return x;
+#endif
+}
+
+// Broadcast a value computed by the leader (after a serial section).
+HD double bcast(const Ctx& c, double v) {
+#if ENGINE_DEVICE
+  __syncthreads();
+  if (c.tid == 0) c.red[0] = v;
+  __syncthreads();
+  double r = c.red[0];
+  __syncthreads();
+  return r;
+#else
+  (void)c;
+  return v;
+#endif
+}
+HD int64_t bcast_i(const Ctx& c, int64_t v) {
+#if ENGINE_DEVICE
+  int64_t* r = reinterpret_cast<int64_t*>(c.red);
+  __syncthreads();
+  if (c.tid == 0) r[0] = v;
+  __syncthreads();
+  int64_t x = r[0];
+  __syncthreads();
+  return x;
+#else
+  (void)c;
+  return v;
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Workspace arena (per filter).  Every thread keeps an identical copy and
+// performs the same allocation sequence, so pointers agree without barriers.
+// ---------------------------------------------------------------------------
+struct Arena {
+  char* base;
+  size_t cap;
+  size_t off;
+  size_t peak;
+
+  template <class T>
+  HD T* alloc(size_t n) {
+    size_t a = (off + 255) & ~(size_t)255;
+    size_t need = a + n * sizeof(T);
+    if (need > cap) return nullptr;
+    off = need;
+    if (off > peak) peak = off;
+    return reinterpret_cast<T*>(base + a);
+  }
+  HD size_t mark() const { return off; }
+  HD void release(size_t m) { off = m; }
+};
+
+#define ALLOC(ptr, T, n, ar) do { (ptr) = (ar).template alloc<T>((size_t)(n)); if (!(ptr)) return ::tg::E_WORKSPACE; } while (0)
+
+// ---------------------------------------------------------------------------
+// parallel helpers
+// ---------------------------------------------------------------------------
+HD void par_fill(const Ctx& c, double* p, int64_t n, double v) {
+  for (int64_t i = c.tid; i < n; i += c.nt) p[i] = v;
+}
+HD void par_copy(const Ctx& c, double* dst, const double* src, int64_t n) {
+  for (int64_t i = c.tid; i < n; i += c.nt) dst[i] = src[i];
+}
+
+}  // namespace tg

@@ -1,0 +1,347 @@
+// Filter stages of Algorithm 3 (filters.py:937-985), one CTA per filter.
+//
+//   stage_prior    initial_pmd_tt            filters.py:497-513
+//   stage_measure  measurement_update (TT) + raw moments
+//                                            filters.py:521-563, 287-333
+//   stage_time     grid_redesign interp+finalize, kernel cross, FFT conv,
+//                  realign cross, finalize   filters.py:799-824, 959-985
+// The tiny host-side geometry between the two (SPD repair, Kalman predict,
+// grid design, corner pull-back) runs in numpy on the host, exactly as the
+// reference computes it.
+#pragma once
+#include "common.cuh"
+#include "tt.cuh"
+#include "models.cuh"
+#include "cross.cuh"
+#include "../../include/ttgbf.h"
+
+namespace tg {
+
+constexpr double MASS_FLOOR = 1e-300;   // filters.py:100
+
+// axis coordinates exactly as numpy builds them: base + step * (i - off)
+HD double axis_value(const ttgbf_axis& a, int i) {
+#if ENGINE_DEVICE
+  return __dadd_rn(a.base, __dmul_rn(a.step, (double)(i - a.off)));
+#else
+  volatile double t = a.step * (double)(i - a.off);
+  return a.base + t;
+#endif
+}
+
+HDN int materialize_axes(const Ctx& c, Arena& ar, int d, const ttgbf_axis* g, double** axes,
+                                AxisGeom* geo, double* steps) {
+  for (int k = 0; k < d; ++k) {
+    ALLOC(axes[k], double, g[k].n, ar);
+    for (int i = c.tid; i < g[k].n; i += c.nt) axes[k][i] = axis_value(g[k], i);
+  }
+  c.sync();
+  for (int k = 0; k < d; ++k) {
+    const double a0 = axes[k][0], a1 = axes[k][g[k].n - 1];
+    geo[k].a0 = a0;
+    geo[k].h = (a1 - a0) / (double)(g[k].n - 1);
+    geo[k].n = g[k].n;
+    steps[k] = geo[k].h;
+  }
+  return OK;
+}
+
+HD double cell_volume(const double* steps, int d) {
+  double v = 1.0;   // np.prod
+  for (int k = 0; k < d; ++k) v *= steps[k];
+  return v;
+}
+
+// packed TT I/O (include/ttgbf.h): header + cores at data + off[k]
+HDN int tt_store(const Ctx& c, const TT& t, ttgbf_tt* hdr, double* data, int64_t cap) {
+  int64_t need = 0;
+  for (int k = 0; k < t.d; ++k) need += t.size(k);
+  if (need > cap) return E_WORKSPACE;
+  int64_t off = 0;
+  for (int k = 0; k < t.d; ++k) {
+    par_copy(c, data + off, t.c[k], t.size(k));
+    off += t.size(k);
+  }
+  if (c.leader()) {
+    hdr->d = t.d;
+    off = 0;
+    for (int k = 0; k < t.d; ++k) { hdr->n[k] = t.n[k]; hdr->off[k] = off; off += t.size(k); }
+    for (int k = 0; k <= t.d; ++k) hdr->r[k] = t.r[k];
+  }
+  c.sync();
+  return OK;
+}
+
+HD TT tt_view(const ttgbf_tt* hdr, double* data) {
+  TT t;
+  t.d = hdr->d;
+  for (int k = 0; k < t.d; ++k) { t.n[k] = hdr->n[k]; t.c[k] = data + hdr->off[k]; }
+  for (int k = 0; k <= t.d; ++k) t.r[k] = hdr->r[k];
+  return t;
+}
+
+// Move a TT that was allocated above `mark` down to `mark` (release the
+// temporaries in between).  Destination addresses never exceed the source.
+HDN int tt_compact(const Ctx& c, Arena& ar, size_t mark, TT& t) {
+  ar.release(mark);
+  TT o;
+  CK(tt_alloc(ar, o, t.d, t.n, t.r));
+  for (int k = 0; k < t.d; ++k) {
+    const int64_t sz = o.size(k);
+    if (o.c[k] == t.c[k]) continue;
+    const int64_t chunk = (int64_t)(t.c[k] - o.c[k]);
+    for (int64_t s0 = 0; s0 < sz; s0 += chunk) {
+      const int64_t s1 = lmin(sz, s0 + chunk);
+      for (int64_t e = s0 + c.tid; e < s1; e += c.nt) o.c[k][e] = t.c[k][e];
+      c.sync();
+    }
+  }
+  c.sync();
+  t = o;
+  return OK;
+}
+
+HD CrossCfg make_cross_cfg(const ttgbf_cross_cfg& x, const int32_t* seeds, int nseeds) {
+  CrossCfg cc;
+  cc.tol = x.tol;
+  cc.max_rank = x.max_rank;
+  cc.max_sweeps = x.max_sweeps;
+  cc.validation_count = x.validation_count;
+  cc.seeds = seeds;
+  cc.nseeds = nseeds;
+  cc.rng.s_lo = x.rng_state[0];
+  cc.rng.s_hi = x.rng_state[1];
+  cc.rng.i_lo = x.rng_state[2];
+  cc.rng.i_hi = x.rng_state[3];
+  cc.rng.has32 = (uint32_t)x.rng_state[4];
+  cc.rng.u32 = (uint32_t)x.rng_state[5];
+  cc.cache_cap = x.cache_cap;
+  return cc;
+}
+
+HD void put_cross(ttgbf_cross_info* o, const CrossInfo& i) {
+  o->achieved = i.achieved;
+  o->calls = i.calls;
+  o->sweeps = i.sweeps;
+  o->converged = i.converged;
+}
+
+// _finalize_tt (filters.py:454-479): round -> mass -> scale -> negative mass
+HDN int finalize_tt(const Ctx& c, Arena& ar, TT& t, const ttgbf_grid_cfg& g, const double* steps,
+                           const int32_t* probes, int nprobes, ttgbf_diag* dg, double* sm) {
+  const int d = t.d;
+  const double dv = cell_volume(steps, d);
+  const size_t mk = ar.mark();
+  double* ws;
+  ALLOC(ws, double, 4 * 1024 + 16, ar);
+  TT r;
+  if (g.normalize_before_round) {
+    const double mass = tt_sum(c, t, ws) * dv;
+    if (c.leader()) dg->mass_before_norm = mass;
+    if (!isfinite(mass) || mass <= MASS_FLOOR) return E_DEGENERATE;
+    tt_scale(c, t, 1.0 / mass);
+    CK(tt_round(c, ar, t, g.round_tol, g.round_max_rank, r, sm));
+  } else {
+    CK(tt_round(c, ar, t, g.round_tol, g.round_max_rank, r, sm));
+    const double mass = tt_sum(c, r, ws) * dv;
+    if (c.leader()) dg->mass_before_norm = mass;
+    if (!isfinite(mass) || mass <= MASS_FLOOR) return E_DEGENERATE;
+    tt_scale(c, r, 1.0 / mass);
+  }
+  double neg = 0.0;
+  CK(tt_negative_mass(c, ar, r, g.densify_guard, probes, nprobes, &neg, sm));
+  if (c.leader()) dg->clipped_mass += neg * dv;
+  c.sync();
+  CK(tt_compact(c, ar, mk, r));
+  t = r;
+  return OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Evaluator specs
+// ---------------------------------------------------------------------------
+HDN int spec_alloc(const Ctx& c, Arena& ar, EvalSpec*& sp) {
+  ALLOC(sp, EvalSpec, 1, ar);
+  (void)c;
+  return OK;
+}
+
+HD void spec_grid(EvalSpec& s, int d, double* const* axes, const ttgbf_axis* g) {
+  s.d = d;
+  for (int k = 0; k < d; ++k) { s.n[k] = g[k].n; s.axes[k] = axes[k]; }
+}
+
+HD void spec_prior(EvalSpec& s, const ttgbf_gauss& p) {
+  s.kind = EV_GAUSS;
+  for (int i = 0; i < MAXD * MAXD; ++i) s.L[i] = p.L[i];
+  for (int i = 0; i < MAXD; ++i) s.mean[i] = p.mean[i];
+  s.log_norm = p.logn;
+}
+
+HD void spec_likelihood(EvalSpec& s, const ttgbf_model& m, const double* z) {
+  s.kind = EV_LIKELIHOOD;
+  s.hkind = m.hkind;
+  s.b = m.b;
+  s.nang = m.nang;
+  for (int i = 0; i < MAXB; ++i) { s.ang[i] = m.ang[i]; s.z[i] = z[i]; }
+  for (int i = 0; i < MAXB * MAXB; ++i) s.Lr[i] = m.Lr[i];
+  for (int i = 0; i < MAXB * MAXD; ++i) s.H[i] = m.H[i];
+  s.log_norm_r = m.logn_r;
+}
+
+HD void spec_kernel(EvalSpec& s, const ttgbf_model& m, const double* steps) {
+  s.kind = EV_KERNEL;
+  for (int i = 0; i < MAXD * MAXD; ++i) { s.F[i] = m.F[i]; s.L[i] = m.Lq[i]; }
+  s.log_norm = m.logn_q;
+  for (int k = 0; k < s.d; ++k) s.steps[k] = steps[k];
+  s.cellvol = cell_volume(steps, s.d);
+}
+
+struct StageSmem {
+  XShared* xs;   // XShared followed by XState
+  double* sm;    // general scratch
+};
+
+// ---------------------------------------------------------------------------
+// initial_pmd_tt (filters.py:497-513)
+// ---------------------------------------------------------------------------
+HDN int stage_prior(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_gauss& prior,
+                           const ttgbf_grid_cfg& gcfg, const ttgbf_cross_cfg& xcfg, const ttgbf_filter_io& io,
+                           const int32_t* probes, int nprobes, ttgbf_tt* hdr, double* state, int64_t cap,
+                           ttgbf_diag* dg, StageSmem S) {
+  const int d = model.d;
+  double* axes[MAXD];
+  AxisGeom geo[MAXD];
+  double steps[MAXD];
+  CK(materialize_axes(c, ar, d, io.cur, axes, geo, steps));
+  EvalSpec* sp;
+  CK(spec_alloc(c, ar, sp));
+  if (c.leader()) { spec_grid(*sp, d, axes, io.cur); spec_prior(*sp, prior); }
+  c.sync();
+  const size_t mk = ar.mark();
+  TT t;
+  CrossInfo ci;
+  CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, nullptr, 0), S.xs, t, &ci, S.sm));
+  if (c.leader()) put_cross(&dg->cross[0], ci);
+  CK(tt_compact(c, ar, mk, t));
+  CK(finalize_tt(c, ar, t, gcfg, steps, probes, nprobes, dg, S.sm));
+  CK(tt_store(c, t, hdr, state, cap));
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// measurement_update (TT branch, filters.py:521-563) + raw moments of the
+// filtering density (filters.py:297-322).  Outlier keeps the prior.
+// ---------------------------------------------------------------------------
+HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_grid_cfg& gcfg,
+                             const ttgbf_cross_cfg& xcfg, const ttgbf_filter_io& io, const int32_t* probes,
+                             int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* hdr, double* state,
+                             int64_t cap, ttgbf_diag* dg, StageSmem S) {
+  const int d = model.d;
+  double* axes[MAXD];
+  AxisGeom geo[MAXD];
+  double steps[MAXD];
+  CK(materialize_axes(c, ar, d, io.cur, axes, geo, steps));
+  TT p = tt_view(hdr, state);
+  if (io.has_z) {
+    EvalSpec* sp;
+    CK(spec_alloc(c, ar, sp));
+    if (c.leader()) { spec_grid(*sp, d, axes, io.cur); spec_likelihood(*sp, model, io.z); }
+    c.sync();
+    const size_t mk = ar.mark();
+    TT lik;
+    CrossInfo ci;
+    CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, seeds, nseeds), S.xs, lik, &ci, S.sm));
+    if (c.leader()) put_cross(&dg->cross[0], ci);
+    CK(tt_compact(c, ar, mk, lik));
+    const size_t mk2 = ar.mark();
+    TT prod;
+    CK(tt_hadamard(c, ar, p, lik, prod));
+    double* ws;
+    ALLOC(ws, double, 4096 + 16, ar);
+    const double mass = tt_sum(c, prod, ws) * cell_volume(steps, d);
+    if (!isfinite(mass) || mass <= MASS_FLOOR) {
+      if (c.leader()) dg->outlier = 1;
+      c.sync();
+    } else {
+      CK(tt_compact(c, ar, mk2, prod));
+      CK(finalize_tt(c, ar, prod, gcfg, steps, probes, nprobes, dg, S.sm));
+      CK(tt_store(c, prod, hdr, state, cap));
+      p = tt_view(hdr, state);
+    }
+  }
+  // raw moments of the filtering density
+  const double* ax[MAXD];
+  for (int k = 0; k < d; ++k) ax[k] = axes[k];
+  double* mom;
+  ALLOC(mom, double, TTGBF_NMOM, ar);
+  CK(tt_moments(c, ar, p, ax, mom));
+  const int nmom = 1 + d + d * (d + 1) / 2;
+  for (int q = c.tid; q < nmom; q += c.nt) dg->raw_moments[q] = mom[q];
+  c.sync();
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// time update of tt_fft_pmf_step (filters.py:958-985)
+// ---------------------------------------------------------------------------
+HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_grid_cfg& gcfg,
+                          const ttgbf_cross_cfg& xcfg, const ttgbf_filter_io& io, const int32_t* probes,
+                          int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* hdr, double* state,
+                          int64_t cap, ttgbf_diag* dg, StageSmem S) {
+  const int d = model.d;
+  double *ac[MAXD], *af[MAXD], *apd[MAXD];
+  AxisGeom gc[MAXD], gf[MAXD], gp[MAXD];
+  double sc[MAXD], sf[MAXD], spd[MAXD];
+  CK(materialize_axes(c, ar, d, io.cur, ac, gc, sc));
+  CK(materialize_axes(c, ar, d, io.filt, af, gf, sf));
+  CK(materialize_axes(c, ar, d, io.pred, apd, gp, spd));
+  EvalSpec* sp;
+  CK(spec_alloc(c, ar, sp));
+  // grid_redesign: interpolate the filtering TT onto the new filtering grid
+  const size_t m0 = ar.mark();
+  TT filt = tt_view(hdr, state);
+  TT shifted;
+  {
+    const double* na[MAXD];
+    for (int k = 0; k < d; ++k) na[k] = af[k];
+    CK(tt_interp(c, ar, filt, gc, na, shifted));
+  }
+  CK(finalize_tt(c, ar, shifted, gcfg, sf, probes, nprobes, dg, S.sm));
+  // kernel cross on the filtering grid
+  if (c.leader()) { spec_grid(*sp, d, af, io.filt); spec_kernel(*sp, model, sf); }
+  c.sync();
+  const size_t m1 = ar.mark();
+  TT ker;
+  CrossInfo ci;
+  CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, nullptr, 0), S.xs, ker, &ci, S.sm));
+  if (c.leader()) put_cross(&dg->cross[1], ci);
+  CK(tt_compact(c, ar, m1, ker));
+  // FFT convolution + rounding
+  TT conv;
+  CK(tt_fft_conv(c, ar, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, conv, S.sm));
+  CK(tt_compact(c, ar, m0, conv));
+  int maxr = 1;
+  for (int k = 0; k <= d; ++k) maxr = imax(maxr, conv.r[k]);
+  if (maxr > 512) return E_ARG;
+  // realign cross on the predictive grid
+  if (c.leader()) {
+    spec_grid(*sp, d, apd, io.pred);
+    sp->kind = EV_REALIGN;
+    for (int i = 0; i < MAXD * MAXD; ++i) sp->Finv[i] = model.Finv[i];
+    sp->conv = conv;
+    for (int k = 0; k < d; ++k) sp->geo[k] = gf[k];
+  }
+  c.sync();
+  const size_t m2 = ar.mark();
+  TT rl;
+  CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, seeds, nseeds), S.xs, rl, &ci, S.sm));
+  if (c.leader()) put_cross(&dg->cross[2], ci);
+  CK(tt_compact(c, ar, m2, rl));
+  CK(finalize_tt(c, ar, rl, gcfg, spd, probes, nprobes, dg, S.sm));
+  CK(tt_store(c, rl, hdr, state, cap));
+  return OK;
+}
+
+}  // namespace tg

@@ -1,0 +1,735 @@
+// Dense FP64 linear algebra for the step engine (CTA-cooperative).
+//
+//  * gemm            C = alpha*op(A) op(B) + beta*C, arbitrary strides, SMEM tiles
+//  * qr_householder  blocked Householder QR (LAPACK dgeqrf semantics: R with
+//                    beta = -sign(alpha)*||x|| diagonal, unit-lower V, tau)
+//  * qr_form_q       explicit thin Q (dorgqr semantics)
+//  * svd_jacobi      one-sided Jacobi SVD (high relative accuracy), sorted
+//  * lstsq_pivoted   QR with column pivoting + rank cut at rcond=eps, the
+//                    algorithm of LAPACK dgelsy that scipy.linalg.lstsq calls in
+//                    the reference cross core solve (tt_algorithms.py:305-307)
+//
+// Matrices are column-major with explicit leading dimension unless stated.
+#pragma once
+#include "common.cuh"
+
+namespace tg {
+
+constexpr double DEPS = 2.220446049250313e-16;
+
+// ---------------------------------------------------------------------------
+// GEMM: C[i,j] = alpha * sum_p A(i,p) B(p,j) + beta * C[i,j]
+// element (i,p) of A at A[i*ars + p*acs]; B(p,j) at B[p*brs + j*bcs];
+// C(i,j) at C[i*crs + j*ccs].  beta == 0 ignores C's previous contents.
+// SMEM: 2 * 16 * 64 doubles (16 KB) taken from `sm`.
+// ---------------------------------------------------------------------------
+HDN void gemm(const Ctx& c, int M, int N, int K, double alpha,
+                     const double* A, int64_t ars, int64_t acs,
+                     const double* B, int64_t brs, int64_t bcs, double beta,
+                     double* C, int64_t crs, int64_t ccs, double* sm) {
+#if ENGINE_DEVICE
+  // 64x64 output tiles, K-tiles of 16 staged in SMEM; 256 threads x (4x4).
+  constexpr int TM = 64, TN = 64, TK = 16;
+  double* As = sm;             // [TK][TM]
+  double* Bs = sm + TK * TM;   // [TK][TN]
+  const int ti = (c.tid % 16) * 4, tj = (c.tid / 16) * 4;
+  for (int i0 = 0; i0 < M; i0 += TM) {
+    for (int j0 = 0; j0 < N; j0 += TN) {
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+      for (int p0 = 0; p0 < K; p0 += TK) {
+        __syncthreads();
+        for (int e = c.tid; e < TK * TM; e += c.nt) {
+          int pp = e / TM, ii = e % TM;
+          int gi = i0 + ii, gp = p0 + pp;
+          As[e] = (gi < M && gp < K) ? A[gi * ars + gp * acs] : 0.0;
+        }
+        for (int e = c.tid; e < TK * TN; e += c.nt) {
+          int pp = e / TN, jj = e % TN;
+          int gj = j0 + jj, gp = p0 + pp;
+          Bs[e] = (gj < N && gp < K) ? B[gp * brs + gj * bcs] : 0.0;
+        }
+        __syncthreads();
+        if (c.tid < 256) {
+#pragma unroll 4
+          for (int pp = 0; pp < TK; ++pp) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) av[a] = As[pp * TM + ti + a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bv[b] = Bs[pp * TN + tj + b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+          }
+        }
+      }
+      if (c.tid < 256) {
+        for (int a = 0; a < 4; ++a) {
+          int gi = i0 + ti + a;
+          if (gi >= M) continue;
+          for (int b = 0; b < 4; ++b) {
+            int gj = j0 + tj + b;
+            if (gj >= N) continue;
+            double* cp = C + gi * crs + gj * ccs;
+            *cp = (beta == 0.0) ? alpha * acc[a][b] : fma(alpha, acc[a][b], beta * (*cp));
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+#else
+  (void)c; (void)sm;
+  for (int i = 0; i < M; ++i)
+    for (int j = 0; j < N; ++j) {
+      double acc = 0.0;
+      for (int p = 0; p < K; ++p) acc = fma(A[i * ars + p * acs], B[p * brs + j * bcs], acc);
+      double* cp = C + i * crs + j * ccs;
+      *cp = (beta == 0.0) ? alpha * acc : fma(alpha, acc, beta * (*cp));
+    }
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Householder reflector (LAPACK dlarfg): given alpha and ||x||, returns tau
+// and beta; the caller scales x by 1/(alpha - beta).
+// ---------------------------------------------------------------------------
+HD void larfg(double alpha, double xnorm, double* tau, double* beta, double* scal) {
+  if (xnorm == 0.0) {
+    *tau = 0.0;
+    *beta = alpha;
+    *scal = 1.0;
+    return;
+  }
+  double b = -copysign(hypot(alpha, xnorm), alpha);
+  *tau = (b - alpha) / b;
+  *scal = 1.0 / (alpha - b);
+  *beta = b;
+}
+
+// Unblocked QR of the panel A[j0:m, j0:j0+jb) (column-major, lda); writes
+// tau[j0..j0+jb).  Each column: norm via block reduction, then the reflector
+// is applied to the remaining panel columns with one fused reduction pass.
+HDN void qr_panel(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb, double* tau) {
+  for (int j = j0; j < j0 + jb && j < m; ++j) {
+    double* col = A + (int64_t)j * lda;
+    double part = 0.0;
+    for (int64_t r = j + 1 + c.tid; r < m; r += c.nt) part = fma(col[r], col[r], part);
+    double xn2 = block_sum(c, part);
+    double alpha = col[j];
+    double t, beta, scal;
+    larfg(alpha, sqrt(xn2), &t, &beta, &scal);
+    // LAPACK computes xnorm with dnrm2 (scaled); sqrt of the sum of squares
+    // agrees to rounding for the magnitudes seen here.
+    for (int64_t r = j + 1 + c.tid; r < m; r += c.nt) col[r] *= scal;
+    c.sync();
+    if (c.leader()) { col[j] = beta; tau[j] = t; }
+    // apply H = I - t v v^T to the remaining panel columns j+1..j0+jb-1
+    const int nrem = j0 + jb - (j + 1);
+    if (nrem > 0 && t != 0.0) {
+      double w[16];
+      for (int q = 0; q < nrem; ++q) w[q] = 0.0;
+      for (int64_t r = j + c.tid; r < m; r += c.nt) {
+        double v = (r == j) ? 1.0 : col[r];
+        for (int q = 0; q < nrem; ++q) w[q] = fma(v, A[(int64_t)(j + 1 + q) * lda + r], w[q]);
+      }
+      for (int q = 0; q < nrem; ++q) w[q] = block_sum(c, w[q]);
+      for (int64_t r = j + c.tid; r < m; r += c.nt) {
+        double v = (r == j) ? 1.0 : col[r];
+        for (int q = 0; q < nrem; ++q) A[(int64_t)(j + 1 + q) * lda + r] -= t * w[q] * v;
+      }
+    }
+    c.sync();
+  }
+}
+
+// Build the upper-triangular block-reflector factor T (jb x jb, col-major ld jb)
+// for V = A[j0:m, j0:j0+jb) (LAPACK dlarft, forward, columnwise).
+HDN void qr_larft(const Ctx& c, const double* A, int64_t lda, int m, int j0, int jb,
+                         const double* tau, double* T, double* sm) {
+  // G = V^T V (upper), computed by per-thread partials then reduced.
+  double* G = sm;  // jb*jb
+  for (int e = c.tid; e < jb * jb; e += c.nt) G[e] = 0.0;
+  c.sync();
+  for (int p = 0; p < jb; ++p) {
+    for (int q = p + 1; q < jb; ++q) {
+      double part = 0.0;
+      for (int64_t r = j0 + q + c.tid; r < m; r += c.nt) {
+        double vp = (r == j0 + p) ? 1.0 : A[(int64_t)(j0 + p) * lda + r];
+        double vq = (r == j0 + q) ? 1.0 : A[(int64_t)(j0 + q) * lda + r];
+        part = fma(vp, vq, part);
+      }
+      double s = block_sum(c, part);
+      if (c.leader()) G[p * jb + q] = s;  // G[p][q] = v_p . v_q
+    }
+  }
+  c.sync();
+  if (c.leader()) {
+    for (int i = 0; i < jb; ++i) {
+      for (int r = 0; r < jb; ++r) T[r + i * jb] = 0.0;
+      T[i + i * jb] = tau[j0 + i];
+      // T(0:i, i) = -tau_i * T(0:i,0:i) * (V(:,0:i)^T v_i)
+      double tmp[16];
+      for (int p = 0; p < i; ++p) tmp[p] = -tau[j0 + i] * G[p * jb + i];
+      for (int p = 0; p < i; ++p) {
+        double s = 0.0;
+        for (int q = p; q < i; ++q) s += T[p + q * jb] * tmp[q];
+        T[p + i * jb] = s;
+      }
+    }
+  }
+  c.sync();
+}
+
+// Apply the block reflector H = I - V T V^T (trans=true: H^T) from the left to
+// C = A[j0:m, c0:c0+nc) (same leading dimension as V's matrix unless given).
+// Mapping: a warp owns 32 consecutive columns (lane = column) and streams all
+// rows; V rows are broadcast.  W = V^T C is accumulated in registers.
+HDN void apply_block_reflector(const Ctx& c, const double* V, int64_t ldv, int m, int j0, int jb,
+                                      const double* T, bool trans, double* Cm, int64_t ldc,
+                                      int c0, int nc, double* sm) {
+  const int nwarps = (c.nt + 31) / 32;
+  const int warp = c.tid >> 5;
+  const int lane = c.tid & 31;
+  double* Ts = sm;  // jb*jb
+  for (int e = c.tid; e < jb * jb; e += c.nt) Ts[e] = T[e];
+  c.sync();
+#if !ENGINE_DEVICE
+  (void)nwarps; (void)warp; (void)lane;
+  for (int cc = 0; cc < nc; ++cc) {
+    double* col = Cm + (int64_t)(c0 + cc) * ldc;
+    double w[16], w2[16];
+    for (int p = 0; p < jb; ++p) {
+      double s = 0.0;
+      for (int64_t r = j0 + p; r < m; ++r) {
+        double v = (r == j0 + p) ? 1.0 : V[(int64_t)(j0 + p) * ldv + r];
+        s = fma(v, col[r], s);
+      }
+      w[p] = s;
+    }
+    for (int p = 0; p < jb; ++p) {
+      double s = 0.0;
+      if (trans) { for (int q = 0; q <= p; ++q) s += Ts[q + p * jb] * w[q]; }
+      else { for (int q = p; q < jb; ++q) s += Ts[p + q * jb] * w[q]; }
+      w2[p] = s;
+    }
+    for (int64_t r = j0; r < m; ++r) {
+      double s = 0.0;
+      for (int p = 0; p < jb && j0 + p <= r; ++p) {
+        double v = (r == j0 + p) ? 1.0 : V[(int64_t)(j0 + p) * ldv + r];
+        s = fma(v, w2[p], s);
+      }
+      col[r] -= s;
+    }
+  }
+#else
+  for (int cb = warp * 32; cb < nc; cb += nwarps * 32) {
+    const int cc = cb + lane;
+    const bool active = cc < nc;
+    double* col = active ? Cm + (int64_t)(c0 + cc) * ldc : Cm;
+    double w[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) w[p] = 0.0;
+    for (int64_t r = j0; r < m; ++r) {
+      double x = active ? col[r] : 0.0;
+      const int pmax = imin(jb, (int)(r - j0) + 1);
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        if (p < pmax) {
+          double v = (r == j0 + p) ? 1.0 : V[(int64_t)(j0 + p) * ldv + r];
+          w[p] = fma(v, x, w[p]);
+        }
+      }
+    }
+    double w2[16];
+#pragma unroll
+    for (int p = 0; p < 16; ++p) {
+      double s = 0.0;
+      if (p < jb) {
+        if (trans) { for (int q = 0; q <= p; ++q) s += Ts[q + p * jb] * w[q]; }
+        else { for (int q = p; q < jb; ++q) s += Ts[p + q * jb] * w[q]; }
+      }
+      w2[p] = s;
+    }
+    if (active) {
+      for (int64_t r = j0; r < m; ++r) {
+        double s = 0.0;
+        const int pmax = imin(jb, (int)(r - j0) + 1);
+#pragma unroll
+        for (int p = 0; p < 16; ++p) {
+          if (p < pmax) {
+            double v = (r == j0 + p) ? 1.0 : V[(int64_t)(j0 + p) * ldv + r];
+            s = fma(v, w2[p], s);
+          }
+        }
+        col[r] -= s;
+      }
+    }
+  }
+#endif
+  c.sync();
+}
+
+constexpr int QR_NB = 16;
+
+// In-place blocked Householder QR of A (m x n, col-major, lda).
+// sm: >= 2*QR_NB*QR_NB + 64 doubles of shared scratch.  T: QR_NB^2 doubles.
+HDN int qr_householder(const Ctx& c, double* A, int64_t lda, int m, int n, double* tau,
+                              double* T, double* sm) {
+  const int k = imin(m, n);
+  for (int j0 = 0; j0 < k; j0 += QR_NB) {
+    const int jb = imin(QR_NB, k - j0);
+    qr_panel(c, A, lda, m, j0, jb, tau);
+    if (j0 + jb < n) {
+      qr_larft(c, A, lda, m, j0, jb, tau, T, sm);
+      apply_block_reflector(c, A, lda, m, j0, jb, T, true, A, lda, j0 + jb, n - (j0 + jb), sm);
+    }
+  }
+  return OK;
+}
+
+// Explicit thin Q (m x k, col-major ldq) from the reflectors stored in A.
+HDN int qr_form_q(const Ctx& c, const double* A, int64_t lda, int m, int k, const double* tau,
+                         double* Q, int64_t ldq, double* T, double* sm) {
+  for (int64_t e = c.tid; e < (int64_t)m * k; e += c.nt) {
+    int64_t j = e / m, i = e % m;
+    Q[j * ldq + i] = (i == j) ? 1.0 : 0.0;
+  }
+  c.sync();
+  const int nblk = (k + QR_NB - 1) / QR_NB;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int j0 = b * QR_NB;
+    const int jb = imin(QR_NB, k - j0);
+    qr_larft(c, A, lda, m, j0, jb, tau, T, sm);
+    apply_block_reflector(c, A, lda, m, j0, jb, T, false, Q, ldq, j0, k - j0, sm);
+  }
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// One-sided Jacobi SVD of X (m x n, col-major ldx), m >= n assumed; X is
+// overwritten by U*S (columns), V (n x n, ld n) accumulates rotations.
+// On return: s[0..n) sorted descending, U columns in X normalised (zero
+// columns stay zero), perm applied to both.  Needs n ints + n doubles ws.
+// Parallel: round-robin tournament, one warp per column pair.
+// ---------------------------------------------------------------------------
+HDN int svd_jacobi(const Ctx& c, double* X, int64_t ldx, int m, int n, double* V, double* s,
+                          int* perm, double* tmp) {
+  for (int64_t e = c.tid; e < (int64_t)n * n; e += c.nt) V[e] = ((e / n) == (e % n)) ? 1.0 : 0.0;
+  c.sync();
+  if (n == 1) {
+    double part = 0.0;
+    for (int64_t r = c.tid; r < m; r += c.nt) part = fma(X[r], X[r], part);
+    double nrm = sqrt(block_sum(c, part));
+    if (c.leader()) { s[0] = nrm; perm[0] = 0; }
+    if (nrm > 0.0)
+      for (int64_t r = c.tid; r < m; r += c.nt) X[r] /= nrm;
+    c.sync();
+    return OK;
+  }
+  const int np = n + (n & 1);            // even number of players
+  const int pairs = np / 2;
+  const int nwarps = imax(1, c.nt / 32);
+  const int warp = c.tid >> 5;
+  const int lane = c.tid & 31;
+  const double tol = DEPS * sqrt((double)m);
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int round = 0; round < np - 1; ++round) {
+#if ENGINE_DEVICE
+      for (int pr = warp; pr < pairs; pr += nwarps) {
+#else
+      for (int pr = 0; pr < pairs; ++pr) {
+#endif
+        // circle method: player 0 fixed, others rotate
+        int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (np - 1);
+        int b = 1 + (np - 2 - pr + round) % (np - 1);
+        if (a >= n || b >= n) continue;
+        if (a > b) { int t = a; a = b; b = t; }
+        double* xa = X + (int64_t)a * ldx;
+        double* xb = X + (int64_t)b * ldx;
+        double al = 0.0, be = 0.0, ga = 0.0;
+#if ENGINE_DEVICE
+        for (int64_t r = lane; r < m; r += 32) {
+          double u = xa[r], v = xb[r];
+          al = fma(u, u, al); be = fma(v, v, be); ga = fma(u, v, ga);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+#else
+        for (int64_t r = 0; r < m; ++r) {
+          double u = xa[r], v = xb[r];
+          al = fma(u, u, al); be = fma(v, v, be); ga = fma(u, v, ga);
+        }
+#endif
+        if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
+        double rel = fabs(ga) / sqrt(al * be);
+        if (rel > off) off = rel;
+        if (rel <= tol) continue;
+        double zeta = (be - al) / (2.0 * ga);
+        double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double cs = 1.0 / sqrt(1.0 + t * t);
+        double sn = cs * t;
+#if ENGINE_DEVICE
+        for (int64_t r = lane; r < m; r += 32) {
+#else
+        for (int64_t r = 0; r < m; ++r) {
+#endif
+          double u = xa[r], v = xb[r];
+          xa[r] = cs * u - sn * v;
+          xb[r] = sn * u + cs * v;
+        }
+        double* va = V + (int64_t)a * n;
+        double* vb = V + (int64_t)b * n;
+#if ENGINE_DEVICE
+        for (int r = lane; r < n; r += 32) {
+#else
+        for (int r = 0; r < n; ++r) {
+#endif
+          double u = va[r], v = vb[r];
+          va[r] = cs * u - sn * v;
+          vb[r] = sn * u + cs * v;
+        }
+      }
+      c.sync();
+    }
+    off = block_max(c, off);
+    if (off <= tol) break;
+  }
+  // norms, normalise, sort descending (stable by index)
+  for (int j = 0; j < n; ++j) {
+    double part = 0.0;
+    const double* xj = X + (int64_t)j * ldx;
+    for (int64_t r = c.tid; r < m; r += c.nt) part = fma(xj[r], xj[r], part);
+    double nr = sqrt(block_sum(c, part));
+    if (c.leader()) tmp[j] = nr;
+  }
+  c.sync();
+  if (c.leader()) {
+    for (int j = 0; j < n; ++j) perm[j] = j;
+    for (int i = 1; i < n; ++i) {  // insertion sort, descending, stable
+      int p = perm[i];
+      int q = i - 1;
+      while (q >= 0 && tmp[perm[q]] < tmp[p]) { perm[q + 1] = perm[q]; --q; }
+      perm[q + 1] = p;
+    }
+    for (int j = 0; j < n; ++j) s[j] = tmp[perm[j]];
+  }
+  c.sync();
+  for (int j = 0; j < n; ++j) {
+    double nr = tmp[j];
+    if (nr > 0.0) {
+      double* xj = X + (int64_t)j * ldx;
+      for (int64_t r = c.tid; r < m; r += c.nt) xj[r] /= nr;
+    }
+  }
+  c.sync();
+  return OK;
+}
+
+// LAPACK dlaic1: one step of incremental condition estimation.
+// job 1: largest singular value, job 2: smallest.  x has length j, w is the
+// new column's top j entries, gamma its diagonal entry.
+HD void laic1(int job, int j, const double* x, double sest, const double* w, double gamma, double* sestpr,
+              double* s, double* c) {
+  const double eps = 1.1102230246251565e-16;   // dlamch('Epsilon')
+  double alpha = 0.0;
+  for (int i = 0; i < j; ++i) alpha += x[i] * w[i];
+  const double absalp = fabs(alpha), absgam = fabs(gamma), absest = fabs(sest);
+  if (job == 1) {
+    if (sest == 0.0) {
+      const double s1 = fmax(absgam, absalp);
+      if (s1 == 0.0) { *s = 0.0; *c = 1.0; *sestpr = 0.0; }
+      else {
+        double ss = alpha / s1, cc = gamma / s1;
+        const double tmp = sqrt(ss * ss + cc * cc);
+        *s = ss / tmp; *c = cc / tmp; *sestpr = s1 * tmp;
+      }
+      return;
+    } else if (absgam <= eps * absest) {
+      *s = 1.0; *c = 0.0;
+      const double tmp = fmax(absest, absalp);
+      const double s1 = absest / tmp, s2 = absalp / tmp;
+      *sestpr = tmp * sqrt(s1 * s1 + s2 * s2);
+      return;
+    } else if (absalp <= eps * absest) {
+      if (absgam <= absest) { *s = 1.0; *c = 0.0; *sestpr = absest; }
+      else { *s = 0.0; *c = 1.0; *sestpr = absgam; }
+      return;
+    } else if (absest <= eps * absalp || absest <= eps * absgam) {
+      const double s1 = absgam, s2 = absalp;
+      if (s1 <= s2) {
+        const double tmp = s1 / s2;
+        const double ss = sqrt(1.0 + tmp * tmp);
+        *sestpr = s2 * ss;
+        *c = (gamma / s2) / ss;
+        *s = copysign(1.0, alpha) / ss;
+      } else {
+        const double tmp = s2 / s1;
+        const double cc = sqrt(1.0 + tmp * tmp);
+        *sestpr = s1 * cc;
+        *s = (alpha / s1) / cc;
+        *c = copysign(1.0, gamma) / cc;
+      }
+      return;
+    } else {
+      const double z1 = alpha / absest, z2 = gamma / absest;
+      const double b = (1.0 - z1 * z1 - z2 * z2) * 0.5;
+      const double cc = z1 * z1;
+      const double t = (b > 0.0) ? cc / (b + sqrt(b * b + cc)) : sqrt(b * b + cc) - b;
+      const double sine = -z1 / t, cosine = -z2 / (1.0 + t);
+      const double tmp = sqrt(sine * sine + cosine * cosine);
+      *s = sine / tmp; *c = cosine / tmp;
+      *sestpr = sqrt(t + 1.0) * absest;
+      return;
+    }
+  }
+  // job == 2
+  if (sest == 0.0) {
+    *sestpr = 0.0;
+    double sine, cosine;
+    if (fmax(absgam, absalp) == 0.0) { sine = 1.0; cosine = 0.0; }
+    else { sine = -gamma; cosine = alpha; }
+    const double s1 = fmax(fabs(sine), fabs(cosine));
+    double ss = sine / s1, cc = cosine / s1;
+    const double tmp = sqrt(ss * ss + cc * cc);
+    *s = ss / tmp; *c = cc / tmp;
+    return;
+  } else if (absgam <= eps * absest) {
+    *s = 0.0; *c = 1.0; *sestpr = absgam;
+    return;
+  } else if (absalp <= eps * absest) {
+    if (absgam <= absest) { *s = 0.0; *c = 1.0; *sestpr = absgam; }
+    else { *s = 1.0; *c = 0.0; *sestpr = absest; }
+    return;
+  } else if (absest <= eps * absalp || absest <= eps * absgam) {
+    const double s1 = absgam, s2 = absalp;
+    if (s1 <= s2) {
+      const double tmp = s1 / s2;
+      const double cc = sqrt(1.0 + tmp * tmp);
+      *sestpr = absest * (tmp / cc);
+      *s = -(gamma / s2) / cc;
+      *c = copysign(1.0, alpha) / cc;
+    } else {
+      const double tmp = s2 / s1;
+      const double ss = sqrt(1.0 + tmp * tmp);
+      *sestpr = absest / ss;
+      *c = (alpha / s1) / ss;
+      *s = -copysign(1.0, gamma) / ss;
+    }
+    return;
+  }
+  const double z1 = alpha / absest, z2 = gamma / absest;
+  const double norma = fmax(1.0 + z1 * z1 + fabs(z1 * z2), fabs(z1 * z2) + z2 * z2);
+  const double test = 1.0 + 2.0 * (z1 - z2) * (z1 + z2);
+  double sine, cosine;
+  if (test >= 0.0) {
+    const double b = (z1 * z1 + z2 * z2 + 1.0) * 0.5;
+    const double cc = z2 * z2;
+    const double t = cc / (b + sqrt(fabs(b * b - cc)));
+    sine = z1 / (1.0 - t);
+    cosine = -z2 / t;
+    *sestpr = sqrt(t + 4.0 * eps * eps * norma) * absest;
+  } else {
+    const double b = (z2 * z2 + z1 * z1 - 1.0) * 0.5;
+    const double cc = z1 * z1;
+    const double t = (b >= 0.0) ? -cc / (b + sqrt(b * b + cc)) : b - sqrt(b * b + cc);
+    sine = -z1 / t;
+    cosine = -z2 / (1.0 + t);
+    *sestpr = sqrt(1.0 + t + 4.0 * eps * eps * norma) * absest;
+  }
+  const double tmp = sqrt(sine * sine + cosine * cosine);
+  *s = sine / tmp;
+  *c = cosine / tmp;
+}
+
+// ---------------------------------------------------------------------------
+// Least squares  A X = B  with A (r x r), B (r x nrhs): the dgelsy algorithm
+// (QR with column pivoting, rank = largest k with |R_kk| > rcond*|R_00|,
+// min-norm solution for rank-deficient A).  A is copied into `W` (r*r), B is
+// read with B(i,j) at B[i + j*ldb] and the solution written to X(i,j) at
+// X[i + j*ldx] (may alias B).  rcond = eps as scipy's default.
+// Workspace: W r*r, W2 r*r, tau r, tau2 r, jpvt r (ints), colnorm r.
+// ---------------------------------------------------------------------------
+HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_c, int r,
+                             const double* B, int64_t ldb, int nrhs, double* X, int64_t ldx,
+                             double* W, double* W2, double* tau, double* tau2, int* jpvt,
+                             double* cn, int* rank_out) {
+  // W(i,j) = A(i,j)
+  for (int64_t e = c.tid; e < (int64_t)r * r; e += c.nt) {
+    int i = (int)(e % r), j = (int)(e / r);
+    W[i + (int64_t)j * r] = A[i * lda_r + j * lda_c];
+  }
+  c.sync();
+  // serial pivoted Householder QR (r <= a few hundred; leader does it with
+  // the other threads helping on the trailing update)
+  if (c.leader())
+    for (int j = 0; j < r; ++j) jpvt[j] = j;
+  c.sync();
+  for (int j = 0; j < r; ++j) {
+    // column norms of the trailing block
+    for (int q = j + c.tid; q < r; q += c.nt) {
+      double s = 0.0;
+      for (int i = j; i < r; ++i) s = fma(W[i + (int64_t)q * r], W[i + (int64_t)q * r], s);
+      cn[q] = s;
+    }
+    c.sync();
+    if (c.leader()) {
+      int best = j;
+      for (int q = j + 1; q < r; ++q)
+        if (cn[q] > cn[best]) best = q;
+      if (best != j) {
+        for (int i = 0; i < r; ++i) {
+          double t = W[i + (int64_t)j * r];
+          W[i + (int64_t)j * r] = W[i + (int64_t)best * r];
+          W[i + (int64_t)best * r] = t;
+        }
+        int t = jpvt[j]; jpvt[j] = jpvt[best]; jpvt[best] = t;
+      }
+      double* col = W + (int64_t)j * r;
+      double xn = 0.0;
+      for (int i = j + 1; i < r; ++i) xn = fma(col[i], col[i], xn);
+      double t2, beta, scal;
+      larfg(col[j], sqrt(xn), &t2, &beta, &scal);
+      for (int i = j + 1; i < r; ++i) col[i] *= scal;
+      col[j] = beta;
+      tau[j] = t2;
+    }
+    c.sync();
+    const double t2 = tau[j];
+    const double* v = W + (int64_t)j * r;
+    if (t2 != 0.0) {
+      for (int q = j + 1 + c.tid; q < r; q += c.nt) {
+        double* cq = W + (int64_t)q * r;
+        double w = cq[j];
+        for (int i = j + 1; i < r; ++i) w = fma(v[i], cq[i], w);
+        w *= t2;
+        cq[j] -= w;
+        for (int i = j + 1; i < r; ++i) cq[i] -= w * v[i];
+      }
+    }
+    c.sync();
+  }
+  // rank by incremental condition estimation (dgelsy with rcond = eps)
+  int rank = 0;
+  if (c.leader()) {
+    double* xmin = cn;            // reuse: column norms no longer needed
+    double* xmax = tau2;          // (tau2 is rewritten below if rank-deficient)
+    double smax = fabs(W[0]);
+    double smin = smax;
+    if (smax != 0.0) {
+      rank = 1;
+      xmin[0] = 1.0;
+      xmax[0] = 1.0;
+      while (rank < r) {
+        const int i = rank;
+        const double* col = W + (int64_t)i * r;
+        double sminpr, s1, c1, smaxpr, s2, c2;
+        laic1(2, rank, xmin, smin, col, col[i], &sminpr, &s1, &c1);
+        laic1(1, rank, xmax, smax, col, col[i], &smaxpr, &s2, &c2);
+        if (!(smaxpr * DEPS <= sminpr)) break;
+        for (int q = 0; q < rank; ++q) { xmin[q] *= s1; xmax[q] *= s2; }
+        xmin[rank] = c1;
+        xmax[rank] = c2;
+        smin = sminpr;
+        smax = smaxpr;
+        ++rank;
+      }
+    }
+    c.ired[0] = rank;
+  }
+  c.sync();
+  rank = c.ired[0];
+  c.sync();
+  if (rank_out) *rank_out = rank;
+  // rank-deficient: QR of [R11 R12]^T (r x rank) -> min-norm solution
+  if (rank > 0 && rank < r) {
+    // W2(i, j) = R(j, i) for j < rank, i in [0, r): (r x rank), col-major ld r
+    for (int64_t e = c.tid; e < (int64_t)r * rank; e += c.nt) {
+      int i = (int)(e % r), j = (int)(e / r);
+      W2[i + (int64_t)j * r] = (i >= j) ? W[j + (int64_t)i * r] : 0.0;
+    }
+    c.sync();
+    if (c.leader()) {
+      for (int j = 0; j < rank; ++j) {
+        double* col = W2 + (int64_t)j * r;
+        double xn = 0.0;
+        for (int i = j + 1; i < r; ++i) xn = fma(col[i], col[i], xn);
+        double t2, beta, scal;
+        larfg(col[j], sqrt(xn), &t2, &beta, &scal);
+        for (int i = j + 1; i < r; ++i) col[i] *= scal;
+        col[j] = beta;
+        tau2[j] = t2;
+        for (int q = j + 1; q < rank; ++q) {
+          double* cq = W2 + (int64_t)q * r;
+          double w = cq[j];
+          for (int i = j + 1; i < r; ++i) w = fma(col[i], cq[i], w);
+          w *= t2;
+          cq[j] -= w;
+          for (int i = j + 1; i < r; ++i) cq[i] -= w * col[i];
+        }
+      }
+    }
+    c.sync();
+  }
+  // per right-hand side: y = Q^T b; solve; permute
+  for (int col = c.tid; col < nrhs; col += c.nt) {
+    double y[160];
+    double* yy = y;
+    // (r <= 150 enforced by the cross: max_rank)
+    for (int i = 0; i < r; ++i) yy[i] = B[i + (int64_t)col * ldb];
+    for (int j = 0; j < r; ++j) {
+      double t2 = tau[j];
+      if (t2 == 0.0) continue;
+      const double* v = W + (int64_t)j * r;
+      double w = yy[j];
+      for (int i = j + 1; i < r; ++i) w = fma(v[i], yy[i], w);
+      w *= t2;
+      yy[j] -= w;
+      for (int i = j + 1; i < r; ++i) yy[i] -= w * v[i];
+    }
+    double sol[160];
+    if (rank == 0) {
+      for (int i = 0; i < r; ++i) sol[i] = 0.0;
+    } else if (rank == r) {
+      for (int i = r - 1; i >= 0; --i) {
+        double s = yy[i];
+        for (int q = i + 1; q < r; ++q) s -= W[i + (int64_t)q * r] * sol[q];
+        sol[i] = s / W[i + (int64_t)i * r];
+      }
+    } else {
+      // [R11 R12] = L2^T Q2^T with W2 = Q2 L2 (L2 upper, rank x rank)
+      // solve L2^T w = y[0:rank] (forward), sol = Q2 [w; 0]
+      double wv[160];
+      for (int i = 0; i < rank; ++i) {
+        double s = yy[i];
+        for (int q = 0; q < i; ++q) s -= W2[q + (int64_t)i * r] * wv[q];
+        wv[i] = s / W2[i + (int64_t)i * r];
+      }
+      for (int i = 0; i < r; ++i) sol[i] = (i < rank) ? wv[i] : 0.0;
+      for (int j = rank - 1; j >= 0; --j) {
+        double t2 = tau2[j];
+        if (t2 == 0.0) continue;
+        const double* v = W2 + (int64_t)j * r;
+        double w = sol[j];
+        for (int i = j + 1; i < r; ++i) w = fma(v[i], sol[i], w);
+        w *= t2;
+        sol[j] -= w;
+        for (int i = j + 1; i < r; ++i) sol[i] -= w * v[i];
+      }
+    }
+    for (int i = 0; i < r; ++i) X[jpvt[i] + (int64_t)col * ldx] = sol[i];
+  }
+  c.sync();
+  return OK;
+}
+
+}  // namespace tg

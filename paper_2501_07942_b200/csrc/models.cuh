@@ -1,0 +1,167 @@
+// Black-box evaluators of the TT-FFT step (device forms of the reference's
+// Python callables):
+//   EV_GAUSS      initial prior pdf on the grid           filters.py:502-505
+//   EV_LIKELIHOOD p(z | x) with angle wrap                 models.py:72-82,146-153
+//   EV_KERNEL     N(disp F^T; 0, Q) * cell volume          filters.py:682-706
+//   EV_REALIGN    conv TT at F^{-1} y (multilinear)        filters.py:969-974
+// Gaussian densities follow models.py:30-69: value = exp(log_norm - |L^-1 r|^2/2)
+// with L the lower Cholesky factor (computed on the host by numpy).
+#pragma once
+#include "common.cuh"
+#include "tt.cuh"
+
+namespace tg {
+
+enum EvalKind : int { EV_GAUSS = 0, EV_LIKELIHOOD = 1, EV_KERNEL = 2, EV_REALIGN = 3 };
+enum HKind : int {
+  H_LINEAR = 0, H_RANGE_BEARING = 1, H_RANGE_BEARING_DEG = 2, H_NORM_BEARING_DEG = 3,
+  H_ABS_FIRST = 4, H_RANGE_AZ_EL = 5, H_CHAIN_QUADRATIC = 6
+};
+
+struct EvalSpec {
+  int kind;
+  int d;
+  int n[MAXD];
+  const double* axes[MAXD];   // coordinates of the black box's grid
+  // Gaussian (prior, or process noise for the kernel): dim == d
+  double L[MAXD * MAXD];      // lower Cholesky, row-major
+  double log_norm;
+  double mean[MAXD];
+  // likelihood
+  int hkind;
+  int b;
+  int nang;
+  int ang[MAXB];
+  double z[MAXB];
+  double Lr[MAXB * MAXB];
+  double log_norm_r;
+  double H[MAXB * MAXD];
+  // kernel
+  double F[MAXD * MAXD];
+  double steps[MAXD];
+  double cellvol;
+  // realign
+  double Finv[MAXD * MAXD];
+  TT conv;
+  AxisGeom geo[MAXD];
+};
+
+// forward substitution with a lower-triangular row-major L (dim m): |L^-1 x|^2
+HD double tri_quad(const double* L, int m, int ld, const double* x) {
+  double y[MAXD > MAXB ? MAXD : MAXB];
+  double q = 0.0;
+  for (int i = 0; i < m; ++i) {
+    double s = x[i];
+    for (int j = 0; j < i; ++j) s -= L[i * ld + j] * y[j];
+    y[i] = s / L[i * ld + i];
+  }
+  for (int i = 0; i < m; ++i) q += y[i] * y[i];
+  return q;
+}
+
+constexpr double RAD2DEG = 57.29577951308232;  // 180/pi as numpy.degrees
+
+// measurement function h(x) -> out[b]
+HD void eval_h(const EvalSpec& s, const double* x, double* out) {
+  const int d = s.d;
+  switch (s.hkind) {
+    case H_LINEAR:
+      for (int i = 0; i < s.b; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < d; ++j) acc += x[j] * s.H[i * MAXD + j];
+        out[i] = acc;
+      }
+      break;
+    case H_RANGE_BEARING:
+      out[0] = hypot(x[0], x[1]);
+      out[1] = atan2(x[1], x[0]);
+      break;
+    case H_RANGE_BEARING_DEG:
+      out[0] = hypot(x[0], x[1]);
+      out[1] = atan2(x[1], x[0]) * RAD2DEG;
+      break;
+    case H_NORM_BEARING_DEG: {
+      double acc = 0.0;
+      for (int j = 0; j < d; ++j) acc += x[j] * x[j];
+      out[0] = sqrt(acc);
+      out[1] = atan2(x[1], x[0]) * RAD2DEG;
+      break;
+    }
+    case H_ABS_FIRST:
+      out[0] = fabs(x[0]);
+      break;
+    case H_RANGE_AZ_EL: {
+      double acc = 0.0;
+      for (int j = 0; j < 3; ++j) acc += x[j] * x[j];
+      out[0] = sqrt(acc);
+      out[1] = atan2(x[1], x[0]);
+      out[2] = atan2(x[2], hypot(x[0], x[1]));
+      break;
+    }
+    case H_CHAIN_QUADRATIC:
+      for (int i = 0; i + 1 < d; ++i) out[i] = x[i] * x[i] + x[i + 1] * x[i + 1];
+      out[d - 1] = x[d - 1];
+      break;
+    default:
+      for (int i = 0; i < s.b; ++i) out[i] = NAN;
+  }
+}
+
+// numpy.mod(a, 360) for the wrap 180 - mod(180 - r, 360)
+HD double np_mod360(double a) {
+  double m = fmod(a, 360.0);
+  if (m != 0.0) {
+    if ((m < 0.0) != (360.0 < 0.0)) m += 360.0;
+  } else {
+    m = copysign(0.0, 360.0);
+  }
+  return m;
+}
+
+// value at one integer multi-index (not used for EV_REALIGN)
+HD double eval_point(const EvalSpec& s, const int32_t* idx) {
+  double x[MAXD];
+  const int d = s.d;
+  switch (s.kind) {
+    case EV_GAUSS: {
+      for (int k = 0; k < d; ++k) x[k] = s.axes[k][idx[k]] - s.mean[k];
+      return exp(s.log_norm - 0.5 * tri_quad(s.L, d, MAXD, x));
+    }
+    case EV_LIKELIHOOD: {
+      for (int k = 0; k < d; ++k) x[k] = s.axes[k][idx[k]];
+      double hz[MAXB];
+      eval_h(s, x, hz);
+      for (int i = 0; i < s.b; ++i) hz[i] = hz[i] - s.z[i];
+      for (int t = 0; t < s.nang; ++t) {
+        const int a = s.ang[t];
+        hz[a] = 180.0 - np_mod360(180.0 - hz[a]);
+      }
+      return exp(s.log_norm_r - 0.5 * tri_quad(s.Lr, s.b, MAXB, hz));
+    }
+    case EV_KERNEL: {
+      double disp[MAXD], q[MAXD];
+      for (int k = 0; k < d; ++k) {
+        const int half = (s.n[k] - 1) / 2;
+        const int sg = idx[k] <= half ? idx[k] : idx[k] - s.n[k];
+        disp[k] = (double)sg * s.steps[k];
+      }
+      for (int i = 0; i < d; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < d; ++j) acc += disp[j] * s.F[i * MAXD + j];
+        q[i] = acc;
+      }
+      return exp(s.log_norm - 0.5 * tri_quad(s.L, d, MAXD, q)) * s.cellvol;
+    }
+    default:
+      return NAN;
+  }
+}
+
+// realign point coordinate k for multi-index idx: (F^{-1} y)_k, y = pred grid node
+HD double realign_coord(const EvalSpec& s, const int32_t* idx, int k) {
+  double acc = 0.0;
+  for (int j = 0; j < s.d; ++j) acc += s.axes[j][idx[j]] * s.Finv[k * MAXD + j];
+  return acc;
+}
+
+}  // namespace tg

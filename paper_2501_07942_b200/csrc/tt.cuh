@@ -1,0 +1,713 @@
+// Tensor-train operations of the step engine (CTA-cooperative, FP64).
+//
+// Layout: core k is a C-order block (r[k], n[k], r[k+1]) -- the reference's
+// layout (tensor_train.py:1-24) -- so core k viewed column-major is the
+// (n[k]*r[k+1]) x r[k] matrix whose thin QR the rounding sweep needs.
+#pragma once
+#include "common.cuh"
+#include "linalg.cuh"
+
+namespace tg {
+
+struct TT {
+  int d;
+  int n[MAXD];
+  int r[MAXD + 1];
+  double* c[MAXD];
+  HD int64_t size(int k) const { return (int64_t)r[k] * n[k] * r[k + 1]; }
+  HD int64_t total() const {
+    int64_t s = 0;
+    for (int k = 0; k < d; ++k) s += size(k);
+    return s;
+  }
+};
+
+HDN int tt_alloc(Arena& ar, TT& t, int d, const int* n, const int* r) {
+  t.d = d;
+  for (int k = 0; k < d; ++k) t.n[k] = n[k];
+  for (int k = 0; k <= d; ++k) t.r[k] = r[k];
+  for (int k = 0; k < d; ++k) ALLOC(t.c[k], double, t.size(k), ar);
+  return OK;
+}
+
+HDN int tt_clone(const Ctx& c, Arena& ar, const TT& src, TT& dst) {
+  CK(tt_alloc(ar, dst, src.d, src.n, src.r));
+  for (int k = 0; k < src.d; ++k) par_copy(c, dst.c[k], src.c[k], src.size(k));
+  c.sync();
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// sum of all entries (tensor_train.py:283-288): v = 1; v = v @ core.sum(1)
+// ---------------------------------------------------------------------------
+HDN double tt_sum(const Ctx& c, const TT& t, double* ws) {
+  // ws: 2 * maxr doubles
+  int maxr = 1;
+  for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
+  double* v = ws;
+  double* w = ws + maxr;
+  if (c.leader()) v[0] = 1.0;
+  c.sync();
+  for (int k = 0; k < t.d; ++k) {
+    const int rl = t.r[k], n = t.n[k], rr = t.r[k + 1];
+    for (int b = c.tid; b < rr; b += c.nt) {
+      double acc = 0.0;
+      for (int a = 0; a < rl; ++a) {
+        const double* p = t.c[k] + (int64_t)a * n * rr + b;
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += p[(int64_t)i * rr];
+        acc = fma(v[a], s, acc);
+      }
+      w[b] = acc;
+    }
+    c.sync();
+    double* tmp = v; v = w; w = tmp;
+  }
+  double res = v[0];
+  c.sync();
+  return res;
+}
+
+// scale core 0 (tensor_train.py:291-295)
+HDN void tt_scale(const Ctx& c, TT& t, double s) {
+  for (int64_t e = c.tid; e < t.size(0); e += c.nt) t.c[0][e] *= s;
+  c.sync();
+}
+
+// ---------------------------------------------------------------------------
+// Moments: for each core the three contractions M_p = sum_i core[:,i,:] x(i)^p
+// (p = 0,1,2), then chain products for mass, d first and d(d+1)/2 second raw
+// moments (filters.py:297-322 with tt_dot of tensor_train.py:269-275).
+// out: [0] = sum (un-normalised), [1..d] first, then second moments (i<=j,
+// row-major upper triangle), all un-normalised (divide by sum).
+// ---------------------------------------------------------------------------
+HDN int tt_moments(const Ctx& c, Arena& ar, const TT& t, const double* const* axes, double* out) {
+  const int d = t.d;
+  size_t mk = ar.mark();
+  double* M[MAXD][3];
+  for (int k = 0; k < d; ++k) {
+    const int rl = t.r[k], n = t.n[k], rr = t.r[k + 1];
+    for (int p = 0; p < 3; ++p) ALLOC(M[k][p], double, (int64_t)rl * rr, ar);
+    for (int64_t e = c.tid; e < (int64_t)rl * rr; e += c.nt) {
+      const int a = (int)(e / rr), b = (int)(e % rr);
+      const double* g = t.c[k] + (int64_t)a * n * rr + b;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double x = axes[k][i];
+        const double v = g[(int64_t)i * rr];
+        s0 += v;
+        s1 = fma(v, x, s1);
+        s2 = fma(v, x * x, s2);
+      }
+      M[k][0][e] = s0;
+      M[k][1][e] = s1;
+      M[k][2][e] = s2;
+    }
+  }
+  c.sync();
+  int maxr = 1;
+  for (int k = 0; k <= d; ++k) maxr = imax(maxr, t.r[k]);
+  const int nmom = 1 + d + d * (d + 1) / 2;
+  double* vec;
+  ALLOC(vec, double, (int64_t)2 * maxr * nmom, ar);
+  // each thread handles whole chains for a subset of moments (tiny work)
+  for (int q = c.tid; q < nmom; q += c.nt) {
+    int pi = -1, pj = -1;
+    if (q >= 1 && q <= d) pi = q - 1;
+    if (q > d) {
+      int idx = q - d - 1;
+      for (int i = 0; i < d; ++i)
+        for (int j = i; j < d; ++j) {
+          if (idx == 0) { pi = i; pj = j; }
+          --idx;
+        }
+    }
+    double* v = vec + (int64_t)2 * maxr * q;
+    double* w = v + maxr;
+    v[0] = 1.0;
+    for (int k = 0; k < d; ++k) {
+      int p = (k == pi) + (k == pj);
+      const double* m = M[k][p];
+      const int rl = t.r[k], rr = t.r[k + 1];
+      for (int b = 0; b < rr; ++b) {
+        double acc = 0.0;
+        for (int a = 0; a < rl; ++a) acc = fma(v[a], m[(int64_t)a * rr + b], acc);
+        w[b] = acc;
+      }
+      double* tmp = v; v = w; w = tmp;
+    }
+    out[q] = v[0];
+  }
+  c.sync();
+  ar.release(mk);
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// Point evaluation.  One warp per point; the running row vector lives in
+// SMEM (per warp 2*maxr doubles at `sm`).  Integer indices (K x d, int32) for
+// tt_eval_many (tensor_train.py:129-158); continuous points with 2-tap
+// multilinear weights for tt_eval_at_points (tt_algorithms.py:721-745).
+// ---------------------------------------------------------------------------
+struct AxisGeom {  // equidistant axis: first value, step, count
+  double a0, h;
+  int n;
+};
+
+// (cell, frac, inside) exactly as tt_algorithms.py:673-684
+HD void axis_cell(const AxisGeom& g, double x, int* cell, double* frac, bool* inside) {
+  const double pos = (x - g.a0) / g.h;
+  const double eps = 1e-9;
+  *inside = (pos >= -eps) && (pos <= (double)(g.n - 1) + eps);
+  double fl = floor(pos);
+  // clip(floor(pos), 0, n-2) as integers (floor of huge values saturates)
+  int ci;
+  if (!(fl >= 0.0)) ci = 0;
+  else if (fl > (double)(g.n - 2)) ci = g.n - 2;
+  else ci = (int)fl;
+  *cell = ci;
+  double f = pos - (double)ci;
+  *frac = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+}
+
+// generic chain evaluation: `slice(k, a, b)` returns core_k[a, i_k, b] for the
+// point; K points; out[K]
+template <class Slice>
+HDN void tt_chain_eval(const Ctx& c, const TT& t, int64_t K, Slice slice, double* out, double* sm) {
+  int maxr = 1;
+  for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
+#if ENGINE_DEVICE
+  const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
+  double* v = sm + (int64_t)warp * 2 * maxr;
+  double* w = v + maxr;
+  for (int64_t p = warp; p < K; p += nwarps) {
+    if (lane == 0) v[0] = 1.0;
+    __syncwarp();
+    double* vv = v;
+    double* ww = w;
+    bool dead = false;
+    for (int k = 0; k < t.d; ++k) {
+      const int rl = t.r[k], rr = t.r[k + 1];
+      if (!slice.prepare(k, p)) { dead = true; break; }
+      for (int b = lane; b < rr; b += 32) {
+        double acc = 0.0;
+        for (int a = 0; a < rl; ++a) acc = fma(vv[a], slice.at(k, a, b), acc);
+        ww[b] = acc;
+      }
+      __syncwarp();
+      double* tmp = vv; vv = ww; ww = tmp;
+    }
+    if (lane == 0) out[p] = dead ? 0.0 : vv[0];
+    __syncwarp();
+  }
+  c.sync();
+#else
+  double* v = sm;
+  double* w = sm + maxr;
+  for (int64_t p = 0; p < K; ++p) {
+    v[0] = 1.0;
+    double* vv = v;
+    double* ww = w;
+    bool dead = false;
+    for (int k = 0; k < t.d; ++k) {
+      const int rl = t.r[k], rr = t.r[k + 1];
+      if (!slice.prepare(k, p)) { dead = true; break; }
+      for (int b = 0; b < rr; ++b) {
+        double acc = 0.0;
+        for (int a = 0; a < rl; ++a) acc = fma(vv[a], slice.at(k, a, b), acc);
+        ww[b] = acc;
+      }
+      double* tmp = vv; vv = ww; ww = tmp;
+    }
+    out[p] = dead ? 0.0 : vv[0];
+  }
+#endif
+}
+
+struct IndexSlice {
+  const TT* t;
+  const int32_t* idx;  // K x d
+  int i;
+  HD bool prepare(int k, int64_t p) { i = idx[p * t->d + k]; return true; }
+  HD double at(int k, int a, int b) const {
+    return t->c[k][((int64_t)a * t->n[k] + i) * t->r[k + 1] + b];
+  }
+};
+
+HDN void tt_eval_idx(const Ctx& c, const TT& t, const int32_t* idx, int64_t K, double* out, double* sm) {
+  IndexSlice s{&t, idx, 0};
+  tt_chain_eval(c, t, K, s, out, sm);
+}
+
+// Evaluation of the TT at continuous points produced by a functor
+// `pt(p, k)` (coordinate k of point p) on axes `geo`; zero outside the hull.
+template <class PointFn>
+struct PointSlice {
+  const TT* t;
+  const AxisGeom* geo;
+  PointFn pt;
+  int cell;
+  double frac;
+  HD bool prepare(int k, int64_t p) {
+    bool inside;
+    axis_cell(geo[k], pt(p, k), &cell, &frac, &inside);
+    return inside;
+  }
+  HD double at(int k, int a, int b) const {
+    const int64_t rr = t->r[k + 1];
+    const double* base = t->c[k] + ((int64_t)a * t->n[k] + cell) * rr + b;
+    // lo * (1 - frac) + hi * frac, as tt_algorithms.py:741
+    return base[0] * (1.0 - frac) + base[rr] * frac;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Hadamard product cores (tensor_train.py:252-266)
+// ---------------------------------------------------------------------------
+HDN int tt_hadamard(const Ctx& c, Arena& ar, const TT& A, const TT& B, TT& out) {
+  int n[MAXD], r[MAXD + 1];
+  for (int k = 0; k < A.d; ++k) n[k] = A.n[k];
+  for (int k = 0; k <= A.d; ++k) r[k] = A.r[k] * B.r[k];
+  CK(tt_alloc(ar, out, A.d, n, r));
+  for (int k = 0; k < A.d; ++k) {
+    const int ra0 = A.r[k], ra1 = A.r[k + 1], rb0 = B.r[k], rb1 = B.r[k + 1], nn = A.n[k];
+    const int64_t tot = out.size(k);
+    for (int64_t e = c.tid; e < tot; e += c.nt) {
+      int64_t q = e;
+      const int bb1 = (int)(q % rb1); q /= rb1;
+      const int aa1 = (int)(q % ra1); q /= ra1;
+      const int i = (int)(q % nn); q /= nn;
+      const int bb0 = (int)(q % rb0); q /= rb0;
+      const int aa0 = (int)q;
+      out.c[k][e] = A.c[k][((int64_t)aa0 * nn + i) * ra1 + aa1] * B.c[k][((int64_t)bb0 * nn + i) * rb1 + bb1];
+    }
+  }
+  c.sync();
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// Separable linear interpolation onto new axes (tt_algorithms.py:687-718)
+// ---------------------------------------------------------------------------
+HDN int tt_interp(const Ctx& c, Arena& ar, const TT& t, const AxisGeom* old_geo,
+                         const double* const* new_axes, TT& out) {
+  CK(tt_alloc(ar, out, t.d, t.n, t.r));
+  for (int k = 0; k < t.d; ++k) {
+    const int rl = t.r[k], n = t.n[k], rr = t.r[k + 1];
+    const int64_t tot = out.size(k);
+    for (int64_t e = c.tid; e < tot; e += c.nt) {
+      const int b = (int)(e % rr);
+      const int j = (int)((e / rr) % n);
+      const int a = (int)(e / ((int64_t)rr * n));
+      int cell;
+      double frac;
+      bool inside;
+      axis_cell(old_geo[k], new_axes[k][j], &cell, &frac, &inside);
+      double v = 0.0;
+      if (inside) {
+        const double* g = t.c[k] + ((int64_t)a * n + cell) * rr + b;
+        v = g[0] * (1.0 - frac) + g[rr] * frac;
+      }
+      out.c[k][e] = v;
+    }
+  }
+  c.sync();
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// Truncation rule (tensor_train.py:165-176)
+// ---------------------------------------------------------------------------
+HD int keep_rank(const double* s, int k, double delta, int cap, double* tail) {
+  int r;
+  if (delta > 0.0) {
+    double acc = 0.0;
+    for (int i = k - 1; i >= 0; --i) { acc += s[i] * s[i]; tail[i] = acc; }
+    const double d2 = delta * delta;
+    r = k;
+    for (int i = 0; i < k; ++i)
+      if (tail[i] <= d2) { r = i; break; }
+    r = imax(r, 1);
+  } else {
+    r = imax(k, 1);
+  }
+  if (cap > 0) r = imin(r, cap);
+  return r;
+}
+
+// SVD of a row-major (m x n) matrix X (read-only): returns U (m x kk, col-major
+// ld m), s (kk), Vt (kk x n, row-major ld n), kk = min(m, n).
+HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, double** U_out,
+                            double** s_out, double** Vt_out, int* kk_out, double* sm) {
+  const int kk = imin(m, n);
+  double *U, *s, *Vt;
+  ALLOC(U, double, (int64_t)m * kk, ar);
+  ALLOC(s, double, kk, ar);
+  ALLOC(Vt, double, (int64_t)kk * n, ar);
+  size_t mk = ar.mark();
+  int* perm;
+  double* tmp;
+  ALLOC(perm, int, kk, ar);
+  ALLOC(tmp, double, kk, ar);
+  // Work on the orientation with more rows than columns: Y (rows >= cols).
+  const bool tall = m >= n;
+  const int yr = tall ? m : n, yc = tall ? n : m;   // yc == kk
+  double* Y;
+  ALLOC(Y, double, (int64_t)yr * yc, ar);
+  if (tall) {  // Y = X (col-major copy)
+    for (int64_t e = c.tid; e < (int64_t)m * n; e += c.nt) {
+      const int i = (int)(e / n), j = (int)(e % n);
+      Y[i + (int64_t)j * m] = X[e];
+    }
+  } else {     // Y = X^T (col-major (n x m)) == X's buffer
+    par_copy(c, Y, X, (int64_t)m * n);
+  }
+  c.sync();
+  // QR preconditioning when Y is much taller than wide
+  double* Z = Y;
+  int zr = yr;
+  double* Qy = nullptr;
+  if (yr > 2 * yc && yc > 1) {
+    double *tau, *T;
+    ALLOC(tau, double, yc, ar);
+    ALLOC(T, double, QR_NB * QR_NB, ar);
+    CK(qr_householder(c, Y, yr, yr, yc, tau, T, sm));
+    ALLOC(Qy, double, (int64_t)yr * yc, ar);
+    CK(qr_form_q(c, Y, yr, yr, yc, tau, Qy, yr, T, sm));
+    ALLOC(Z, double, (int64_t)yc * yc, ar);
+    for (int64_t e = c.tid; e < (int64_t)yc * yc; e += c.nt) {
+      const int i = (int)(e % yc), j = (int)(e / yc);
+      Z[e] = (i <= j) ? Y[i + (int64_t)j * yr] : 0.0;
+    }
+    c.sync();
+    zr = yc;
+  }
+  double* Vj;
+  ALLOC(Vj, double, (int64_t)yc * yc, ar);
+  CK(svd_jacobi(c, Z, zr, zr, yc, Vj, s, perm, tmp));
+  // Left vectors of Y: Uy = (Qy *) Z[:, perm]  (yr x kk);  right: Vj[:, perm]
+  double* Uy;
+  ALLOC(Uy, double, (int64_t)yr * kk, ar);
+  if (Qy) {
+    double* Zp;
+    ALLOC(Zp, double, (int64_t)zr * kk, ar);
+    for (int64_t e = c.tid; e < (int64_t)zr * kk; e += c.nt) {
+      const int i = (int)(e % zr), j = (int)(e / zr);
+      Zp[e] = Z[i + (int64_t)perm[j] * zr];
+    }
+    c.sync();
+    gemm(c, yr, kk, zr, 1.0, Qy, 1, yr, Zp, 1, zr, 0.0, Uy, 1, yr, sm);
+  } else {
+    for (int64_t e = c.tid; e < (int64_t)yr * kk; e += c.nt) {
+      const int i = (int)(e % yr), j = (int)(e / yr);
+      Uy[e] = Z[i + (int64_t)perm[j] * zr];
+    }
+    c.sync();
+  }
+  if (tall) {  // X = Uy S Vj^T : U = Uy, Vt[j, :] = Vj[:, perm[j]]
+    par_copy(c, U, Uy, (int64_t)m * kk);
+    for (int64_t e = c.tid; e < (int64_t)kk * n; e += c.nt) {
+      const int j = (int)(e / n), q = (int)(e % n);
+      Vt[e] = Vj[q + (int64_t)perm[j] * yc];
+    }
+  } else {     // X^T = Uy S Vj^T -> X = Vj S Uy^T : U = Vj[:, perm], Vt = Uy^T
+    for (int64_t e = c.tid; e < (int64_t)m * kk; e += c.nt) {
+      const int i = (int)(e % m), j = (int)(e / m);
+      U[e] = Vj[i + (int64_t)perm[j] * yc];
+    }
+    for (int64_t e = c.tid; e < (int64_t)kk * n; e += c.nt) {
+      const int j = (int)(e / n), q = (int)(e % n);
+      Vt[e] = Uy[q + (int64_t)j * yr];
+    }
+  }
+  c.sync();
+  ar.release(mk);
+  *U_out = U;
+  *s_out = s;
+  *Vt_out = Vt;
+  *kk_out = kk;
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// TT rounding (tensor_train.py:327-360): right-to-left Householder QR, then
+// left-to-right truncated SVD with the reference's rule and sweep direction.
+// The result is written into `out` (allocated here, after the temporaries are
+// released, so the caller's arena holds only the output).
+// ---------------------------------------------------------------------------
+HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT& out, double* sm) {
+  const int d = in.d;
+  if (d == 1) return tt_clone(c, ar, in, out);
+  size_t mk0 = ar.mark();
+  TT w;
+  CK(tt_clone(c, ar, in, w));
+  double* T;
+  ALLOC(T, double, QR_NB * QR_NB, ar);
+  for (int k = d - 1; k >= 1; --k) {
+    const int rl = w.r[k], n = w.n[k], rr = w.r[k + 1];
+    const int m = n * rr;
+    const int kk = imin(m, rl);
+    size_t mk = ar.mark();
+    double *tau, *Q, *Rm;
+    ALLOC(tau, double, kk, ar);
+    CK(qr_householder(c, w.c[k], m, m, rl, tau, T, sm));
+    ALLOC(Rm, double, (int64_t)kk * rl, ar);   // R (kk x rl) row-major
+    for (int64_t e = c.tid; e < (int64_t)kk * rl; e += c.nt) {
+      const int i = (int)(e / rl), j = (int)(e % rl);
+      Rm[e] = (i <= j) ? w.c[k][i + (int64_t)j * m] : 0.0;
+    }
+    ALLOC(Q, double, (int64_t)m * kk, ar);
+    c.sync();
+    CK(qr_form_q(c, w.c[k], m, m, kk, tau, Q, m, T, sm));
+    // new core k = Q^T reshaped (kk, n, rr): Q col-major (m x kk) == C-order
+    par_copy(c, w.c[k], Q, (int64_t)m * kk);
+    // core k-1 <- core k-1 x_3 R^T : (rpp*n', rl) @ R^T (rl x kk)
+    const int rpp = w.r[k - 1], np_ = w.n[k - 1];
+    double* nc;
+    ALLOC(nc, double, (int64_t)rpp * np_ * kk, ar);
+    c.sync();
+    gemm(c, rpp * np_, kk, rl, 1.0, w.c[k - 1], rl, 1, Rm, 1, rl, 0.0, nc, kk, 1, sm);
+    // cores may only shrink: copy back into the existing buffers
+    par_copy(c, w.c[k - 1], nc, (int64_t)rpp * np_ * kk);
+    c.sync();
+    w.r[k] = kk;
+    ar.release(mk);
+  }
+  // Frobenius norm of core 0
+  double part = 0.0;
+  for (int64_t e = c.tid; e < w.size(0); e += c.nt) part = fma(w.c[0][e], w.c[0][e], part);
+  const double nrm = sqrt(block_sum(c, part));
+  if (nrm == 0.0) {
+    ar.release(mk0);
+    int n1[MAXD], r1[MAXD + 1];
+    for (int k = 0; k < d; ++k) n1[k] = in.n[k];
+    for (int k = 0; k <= d; ++k) r1[k] = 1;
+    CK(tt_alloc(ar, out, d, n1, r1));
+    for (int k = 0; k < d; ++k) par_fill(c, out.c[k], out.n[k], 0.0);
+    c.sync();
+    return OK;
+  }
+  const double delta = tol * nrm / sqrt((double)(d - 1));
+  for (int k = 0; k < d - 1; ++k) {
+    const int rl = w.r[k], n = w.n[k], rr = w.r[k + 1];
+    const int m = rl * n;
+    size_t mk = ar.mark();
+    double *U, *s, *Vt;
+    int kk;
+    CK(svd_rowmajor(c, ar, w.c[k], m, rr, &U, &s, &Vt, &kk, sm));
+    double* tail;
+    ALLOC(tail, double, kk, ar);
+    int rnew = 0;
+    if (c.leader()) rnew = keep_rank(s, kk, delta, cap, tail);
+    rnew = (int)bcast_i(c, rnew);
+    // core k = U[:, :rnew] (C-order (rl, n, rnew))
+    for (int64_t e = c.tid; e < (int64_t)m * rnew; e += c.nt) {
+      const int64_t i = e / rnew;
+      const int j = (int)(e % rnew);
+      w.c[k][e] = U[i + (int64_t)j * m];
+    }
+    // carry = s[:rnew, None] * Vt[:rnew]  (rnew x rr); core k+1 <- carry @ core
+    double* carry;
+    ALLOC(carry, double, (int64_t)rnew * rr, ar);
+    for (int64_t e = c.tid; e < (int64_t)rnew * rr; e += c.nt) carry[e] = s[e / rr] * Vt[e];
+    const int n2 = w.n[k + 1], r2 = w.r[k + 2];
+    double* nc;
+    ALLOC(nc, double, (int64_t)rnew * n2 * r2, ar);
+    c.sync();
+    gemm(c, rnew, n2 * r2, rr, 1.0, carry, rr, 1, w.c[k + 1], (int64_t)n2 * r2, 1, 0.0, nc,
+         (int64_t)n2 * r2, 1, sm);
+    par_copy(c, w.c[k + 1], nc, (int64_t)rnew * n2 * r2);
+    c.sync();
+    w.r[k + 1] = rnew;
+    ar.release(mk);
+  }
+  // move the result to the front of the released region
+  TT res;
+  res.d = d;
+  for (int k = 0; k < d; ++k) res.n[k] = w.n[k];
+  for (int k = 0; k <= d; ++k) res.r[k] = w.r[k];
+  // w's buffers sit right after mk0; compact in order (sizes only shrank)
+  ar.release(mk0);
+  CK(tt_alloc(ar, out, d, res.n, res.r));
+  for (int k = 0; k < d; ++k) {
+    // out.c[k] <= w.c[k] in address (same allocation order, smaller sizes):
+    // forward copy is safe in a serial pass, so do it in chunks with syncs.
+    const int64_t sz = out.size(k);
+    if (out.c[k] == w.c[k]) continue;
+    const int64_t chunk = (int64_t)(w.c[k] - out.c[k]);
+    for (int64_t s0 = 0; s0 < sz; s0 += chunk) {
+      const int64_t s1 = lmin(sz, s0 + chunk);
+      for (int64_t e = s0 + c.tid; e < s1; e += c.nt) out.c[k][e] = w.c[k][e];
+      c.sync();
+    }
+  }
+  c.sync();
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// FFT convolution in TT form (tt_algorithms.py:642-666): transforms of both
+// TTs' mode fibres, Kronecker product in the frequency domain, inverse
+// transform (real part, using Hermitian symmetry), then tt_round.
+// ---------------------------------------------------------------------------
+HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double tol, int cap,
+                           TT& out, double* sm) {
+  const int d = K.d;
+  size_t mk0 = ar.mark();
+  TT P;
+  {
+    int n[MAXD], r[MAXD + 1];
+    for (int k = 0; k < d; ++k) n[k] = K.n[k];
+    for (int k = 0; k <= d; ++k) r[k] = K.r[k] * W.r[k];
+    CK(tt_alloc(ar, P, d, n, r));
+  }
+  for (int k = 0; k < d; ++k) {
+    const int n = K.n[k];
+    const int nh = (n - 1) / 2;   // n odd
+    size_t mk = ar.mark();
+    double *cs, *sn;
+    ALLOC(cs, double, n, ar);
+    ALLOC(sn, double, n, ar);
+    for (int q = c.tid; q < n; q += c.nt) {
+      // e^{-2 pi i q / n}: forward twiddles; inverse uses the conjugate
+      const double ang = 2.0 * 3.14159265358979323846 * (double)q / (double)n;
+      cs[q] = cos(ang);
+      sn[q] = sin(ang);
+    }
+    // spectra: fiber-major layout [a][b][omega] for omega in [0, nh]
+    const int ka = K.r[k], kb = K.r[k + 1], wa = W.r[k], wb = W.r[k + 1];
+    double *Kr, *Ki, *Wr, *Wi;
+    ALLOC(Kr, double, (int64_t)ka * kb * (nh + 1), ar);
+    ALLOC(Ki, double, (int64_t)ka * kb * (nh + 1), ar);
+    ALLOC(Wr, double, (int64_t)wa * wb * (nh + 1), ar);
+    ALLOC(Wi, double, (int64_t)wa * wb * (nh + 1), ar);
+    c.sync();
+    for (int64_t e = c.tid; e < (int64_t)ka * kb * (nh + 1); e += c.nt) {
+      const int om = (int)(e % (nh + 1));
+      const int64_t f = e / (nh + 1);
+      const int a = (int)(f / kb), b = (int)(f % kb);
+      double re = 0.0, im = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double x = K.c[k][((int64_t)a * n + i) * kb + b];
+        const int q = (int)(((int64_t)om * i) % n);
+        re = fma(x, cs[q], re);
+        im = fma(-x, sn[q], im);
+      }
+      Kr[e] = re;
+      Ki[e] = im;
+    }
+    for (int64_t e = c.tid; e < (int64_t)wa * wb * (nh + 1); e += c.nt) {
+      const int om = (int)(e % (nh + 1));
+      const int64_t f = e / (nh + 1);
+      const int a = (int)(f / wb), b = (int)(f % wb);
+      double re = 0.0, im = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const double x = W.c[k][((int64_t)a * n + i) * wb + b];
+        const int q = (int)(((int64_t)om * i) % n);
+        re = fma(x, cs[q], re);
+        im = fma(-x, sn[q], im);
+      }
+      Wr[e] = re;
+      Wi[e] = im;
+    }
+    c.sync();
+    // product fibre (a1 a2, j, b1 b2) = (1/n) [P0 + 2 sum_{om=1..nh} Re(P_om e^{+i 2pi om j/n})]
+    const int64_t nfib = (int64_t)ka * wa * kb * wb;
+    const double inv_n = 1.0 / (double)n;
+    const int pr = P.r[k + 1];
+    for (int64_t f = c.tid; f < nfib; f += c.nt) {
+      int64_t q = f;
+      const int b2 = (int)(q % wb); q /= wb;
+      const int b1 = (int)(q % kb); q /= kb;
+      const int a2 = (int)(q % wa); q /= wa;
+      const int a1 = (int)q;
+      const double* kr = Kr + ((int64_t)a1 * kb + b1) * (nh + 1);
+      const double* ki = Ki + ((int64_t)a1 * kb + b1) * (nh + 1);
+      const double* wr = Wr + ((int64_t)a2 * wb + b2) * (nh + 1);
+      const double* wi = Wi + ((int64_t)a2 * wb + b2) * (nh + 1);
+      double pre[80], pim[80];   // nh + 1 <= 80 (n <= 159)
+      for (int om = 0; om <= nh; ++om) {
+        pre[om] = kr[om] * wr[om] - ki[om] * wi[om];
+        pim[om] = kr[om] * wi[om] + ki[om] * wr[om];
+      }
+      const int row = a1 * wa + a2, col = b1 * wb + b2;
+      double* dst = P.c[k] + (int64_t)row * n * pr + col;
+      for (int j = 0; j < n; ++j) {
+        double acc = 0.0;
+        for (int om = 1; om <= nh; ++om) {
+          const int qq = (int)(((int64_t)om * j) % n);
+          acc = fma(pre[om], cs[qq], acc);
+          acc = fma(-pim[om], sn[qq], acc);
+        }
+        dst[(int64_t)j * pr] = (pre[0] + 2.0 * acc) * inv_n;
+      }
+    }
+    c.sync();
+    ar.release(mk);
+  }
+  TT R;
+  CK(tt_round(c, ar, P, tol, cap, R, sm));
+  // R sits after P in the arena: move it down over P
+  ar.release(mk0);
+  TT o;
+  CK(tt_alloc(ar, o, d, R.n, R.r));
+  for (int k = 0; k < d; ++k) {
+    const int64_t sz = o.size(k);
+    const int64_t chunk = (int64_t)(R.c[k] - o.c[k]);
+    for (int64_t s0 = 0; s0 < sz; s0 += chunk) {
+      const int64_t s1 = lmin(sz, s0 + chunk);
+      for (int64_t e = s0 + c.tid; e < s1; e += c.nt) o.c[k][e] = R.c[k][e];
+      c.sync();
+    }
+  }
+  out = o;
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
+// Negative mass (filters.py:427-436): exact by full evaluation when the grid
+// has at most `guard` points, else the mean of max(-v,0) over the fixed
+// probe cells times the point count.  Returns the un-scaled sum or mean.
+// ---------------------------------------------------------------------------
+HDN int tt_negative_mass(const Ctx& c, Arena& ar, const TT& t, int64_t guard, const int32_t* probes,
+                                int nprobes, double* result, double* sm) {
+  int64_t total = 1;
+  bool big = false;
+  for (int k = 0; k < t.d; ++k) {
+    if (total > guard) big = true;
+    total *= t.n[k];
+    if (total > guard) big = true;
+  }
+  size_t mk = ar.mark();
+  if (!big) {
+    // dense chain: M (prod n_<k, r_k) -> M @ core_k.reshape(r_k, n_k r_{k+1})
+    double* M;
+    ALLOC(M, double, (int64_t)t.n[0] * t.r[1], ar);
+    par_copy(c, M, t.c[0], t.size(0));
+    c.sync();
+    int64_t rows = t.n[0];
+    for (int k = 1; k < t.d; ++k) {
+      const int rl = t.r[k], n = t.n[k], rr = t.r[k + 1];
+      double* M2;
+      ALLOC(M2, double, rows * n * rr, ar);
+      gemm(c, (int)rows, n * rr, rl, 1.0, M, rl, 1, t.c[k], (int64_t)n * rr, 1, 0.0, M2, (int64_t)n * rr, 1, sm);
+      M = M2;
+      rows *= n;
+    }
+    double part = 0.0;
+    for (int64_t e = c.tid; e < rows; e += c.nt)
+      if (M[e] < 0.0) part -= M[e];
+    *result = block_sum(c, part);
+  } else {
+    double* vals;
+    ALLOC(vals, double, nprobes, ar);
+    tt_eval_idx(c, t, probes, nprobes, vals, sm);
+    double part = 0.0;
+    for (int e = c.tid; e < nprobes; e += c.nt) part += fmax(-vals[e], 0.0);
+    *result = block_sum(c, part) / (double)nprobes * (double)total;
+  }
+  ar.release(mk);
+  return OK;
+}
+
+}  // namespace tg
