@@ -110,6 +110,14 @@ typedef struct {
   ttgbf_cross_info cross[3];     /* prior|likelihood, kernel, realign */
   double raw_moments[TTGBF_NMOM];/* sum, first (d), second (i<=j), un-normalised */
   int64_t ws_peak;               /* bytes of workspace used */
+  /* shape log: ranks of 0 input TT, 1 likelihood cross TT, 2 filtering TT,
+   * 3 shifted TT, 4 kernel cross TT, 5 rounded convolution, 6 realign cross
+   * TT, 7 output TT (used for the algorithmic FLOP count) */
+  int32_t ranks[8][TTGBF_MAXD + 1];
+  /* SM clock cycles of the stage sections (CTA leader): 0 likelihood cross,
+   * 1 Hadamard+finalize, 2 moments, 3 interp+finalize, 4 kernel cross,
+   * 5 FFT conv+round, 6 realign cross, 7 final finalize */
+  int64_t cycles[8];
 } ttgbf_diag;
 
 /* Model constants (StateSpaceModel, models.py:85-153).  Matrices row-major

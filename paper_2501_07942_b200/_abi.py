@@ -32,7 +32,7 @@ CROSS_INFO = np.dtype([("achieved", "f8"), ("calls", "i8"), ("sweeps", "i4"), ("
                       align=True)
 DIAG = np.dtype([("status", "i4"), ("outlier", "i4"), ("mass_before_norm", "f8"),
                  ("clipped_mass", "f8"), ("cross", CROSS_INFO, 3), ("raw_moments", "f8", NMOM),
-                 ("ws_peak", "i8")], align=True)
+                 ("ws_peak", "i8"), ("ranks", "i4", (8, MAXD + 1)), ("cycles", "i8", 8)], align=True)
 MODEL = np.dtype([("d", "i4"), ("b", "i4"), ("hkind", "i4"), ("nang", "i4"), ("ang", "i4", MAXB),
                   ("F", "f8", MAXD * MAXD), ("Finv", "f8", MAXD * MAXD), ("Lq", "f8", MAXD * MAXD),
                   ("logn_q", "f8"), ("Lr", "f8", MAXB * MAXB), ("logn_r", "f8"),

@@ -67,6 +67,9 @@ class CudaBackend:
     def zero(self, buf: DeviceBuffer) -> None:
         buf.t.zero_()
 
+    def event(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
     def sync(self) -> None:
         self.torch.cuda.synchronize(self.device)
 

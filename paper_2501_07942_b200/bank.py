@@ -160,13 +160,29 @@ class FilterBank:
         self.diag_dev = backend.empty(n * _abi.DIAG.itemsize)
         self.grids: list[geo.Axes | None] = [None] * n
         self.alive = np.zeros(n, dtype=bool)
+        self.timeline = None          # list of (name, start_event, end_event) when profiling
+        self.bytes_h2d = 0
+        self.bytes_d2h = 0
 
     # -- helpers ----------------------------------------------------------------
     def _push_io(self):
         self.be.upload_into(self.io_dev, self.io)
+        self.bytes_h2d += self.io.nbytes
 
     def _diag(self) -> np.ndarray:
+        self.bytes_d2h += self.count * _abi.DIAG.itemsize
         return self.be.download(self.diag_dev, _abi.DIAG, self.count)
+
+    def _launch(self, name, fn, *args):
+        ev = None
+        if self.timeline is not None and hasattr(self.be, "event"):
+            ev = (self.be.event(), self.be.event())
+            ev[0].record(self.be.stream)
+        rc = fn(*args)
+        if ev is not None:
+            ev[1].record(self.be.stream)
+            self.timeline.append((name, ev[0], ev[1]))
+        self.be.check(rc, name)
 
     def _ptrs(self):
         return (self.probes.ptr, len(self.probes_np), self.seeds.ptr, len(self.seeds_np))
@@ -187,11 +203,10 @@ class FilterBank:
             self.io["cur"][i] = grid.device()
             self.grids[i] = grid
         self._push_io()
-        rc = self.lib.ttgbf_filter_prior(self.model.ptr, prior.ptr, self.gcfg, self.xcfg, self.io_dev.ptr,
-                                         self.count, self.probes.ptr, len(self.probes_np), self.hdr.ptr,
-                                         self.state.ptr, self.cfg.state_doubles, self.ws.ptr,
-                                         self.cfg.ws_bytes, self.diag_dev.ptr, self.be.stream_ptr)
-        self.be.check(rc, "ttgbf_filter_prior")
+        self._launch("ttgbf_filter_prior", self.lib.ttgbf_filter_prior, self.model.ptr, prior.ptr, self.gcfg,
+                     self.xcfg, self.io_dev.ptr, self.count, self.probes.ptr, len(self.probes_np), self.hdr.ptr,
+                     self.state.ptr, self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes, self.diag_dev.ptr,
+                     self.be.stream_ptr)
         dg = self._diag()
         ok = dg["status"][which] == 0
         self.alive[which] = ok
@@ -202,14 +217,13 @@ class FilterBank:
         z = np.atleast_2d(np.asarray(z, dtype=float))
         self.io["active"] = self.alive.astype(np.int32)
         self.io["z"][:, :self.b] = z
+        self.bytes_h2d += z.nbytes
         self.io["has_z"] = 1 if has_z is None else np.asarray(has_z, dtype=np.int32)
         self._push_io()
         pr, npr, sd, nsd = self._ptrs()
-        rc = self.lib.ttgbf_filter_measure(self.model.ptr, self.gcfg, self.xcfg, self.io_dev.ptr, self.count,
-                                           pr, npr, sd, nsd, self.hdr.ptr, self.state.ptr,
-                                           self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes,
-                                           self.diag_dev.ptr, self.be.stream_ptr)
-        self.be.check(rc, "ttgbf_filter_measure")
+        self._launch("ttgbf_filter_measure", self.lib.ttgbf_filter_measure, self.model.ptr, self.gcfg, self.xcfg,
+                     self.io_dev.ptr, self.count, pr, npr, sd, nsd, self.hdr.ptr, self.state.ptr,
+                     self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes, self.diag_dev.ptr, self.be.stream_ptr)
         return self._diag()
 
     def geometry(self, dg):
@@ -240,11 +254,9 @@ class FilterBank:
         self.io["active"] = act
         self._push_io()
         pr, npr, sd, nsd = self._ptrs()
-        rc = self.lib.ttgbf_filter_time_update(self.model.ptr, self.gcfg, self.xcfg, self.io_dev.ptr,
-                                               self.count, pr, npr, sd, nsd, self.hdr.ptr, self.state.ptr,
-                                               self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes,
-                                               self.diag_dev.ptr, self.be.stream_ptr)
-        self.be.check(rc, "ttgbf_filter_time_update")
+        self._launch("ttgbf_filter_time_update", self.lib.ttgbf_filter_time_update, self.model.ptr, self.gcfg,
+                     self.xcfg, self.io_dev.ptr, self.count, pr, npr, sd, nsd, self.hdr.ptr, self.state.ptr,
+                     self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes, self.diag_dev.ptr, self.be.stream_ptr)
         dg = self._diag()
         for i, (st, payload) in geom.items():
             if st == "ok" and dg["status"][i] == 0:

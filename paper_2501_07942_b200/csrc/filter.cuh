@@ -19,6 +19,18 @@ namespace tg {
 
 constexpr double MASS_FLOOR = 1e-300;   // filters.py:100
 
+HD int64_t clk() {
+#if ENGINE_DEVICE
+  return (int64_t)clock64();
+#else
+  return 0;
+#endif
+}
+
+HD void log_ranks(ttgbf_diag* dg, int slot, const TT& t) {
+  for (int k = 0; k <= TTGBF_MAXD; ++k) dg->ranks[slot][k] = k <= t.d ? t.r[k] : 0;
+}
+
 // axis coordinates exactly as numpy builds them: base + step * (i - off)
 HD double axis_value(const ttgbf_axis& a, int i) {
 #if ENGINE_DEVICE
@@ -244,6 +256,8 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
   double steps[MAXD];
   CK(materialize_axes(c, ar, d, io.cur, axes, geo, steps));
   TT p = tt_view(hdr, state);
+  if (c.leader()) log_ranks(dg, 0, p);
+  int64_t t0 = clk();
   if (io.has_z) {
     EvalSpec* sp;
     CK(spec_alloc(c, ar, sp));
@@ -253,8 +267,11 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
     TT lik;
     CrossInfo ci;
     CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, seeds, nseeds), S.xs, lik, &ci, S.sm));
-    if (c.leader()) put_cross(&dg->cross[0], ci);
+    if (c.leader()) { put_cross(&dg->cross[0], ci); log_ranks(dg, 1, lik); }
     CK(tt_compact(c, ar, mk, lik));
+    const int64_t t1 = clk();
+    if (c.leader()) dg->cycles[0] = t1 - t0;
+    t0 = t1;
     const size_t mk2 = ar.mark();
     TT prod;
     CK(tt_hadamard(c, ar, p, lik, prod));
@@ -271,6 +288,8 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
       p = tt_view(hdr, state);
     }
   }
+  if (c.leader()) { log_ranks(dg, 2, p); dg->cycles[1] = clk() - t0; }
+  t0 = clk();
   // raw moments of the filtering density
   const double* ax[MAXD];
   for (int k = 0; k < d; ++k) ax[k] = axes[k];
@@ -279,6 +298,7 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
   CK(tt_moments(c, ar, p, ax, mom));
   const int nmom = 1 + d + d * (d + 1) / 2;
   for (int q = c.tid; q < nmom; q += c.nt) dg->raw_moments[q] = mom[q];
+  if (c.leader()) dg->cycles[2] = clk() - t0;
   c.sync();
   return OK;
 }
@@ -303,12 +323,15 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   const size_t m0 = ar.mark();
   TT filt = tt_view(hdr, state);
   TT shifted;
+  int64_t t0 = clk();
   {
     const double* na[MAXD];
     for (int k = 0; k < d; ++k) na[k] = af[k];
     CK(tt_interp(c, ar, filt, gc, na, shifted));
   }
   CK(finalize_tt(c, ar, shifted, gcfg, sf, probes, nprobes, dg, S.sm));
+  if (c.leader()) { log_ranks(dg, 3, shifted); dg->cycles[3] = clk() - t0; }
+  t0 = clk();
   // kernel cross on the filtering grid
   if (c.leader()) { spec_grid(*sp, d, af, io.filt); spec_kernel(*sp, model, sf); }
   c.sync();
@@ -316,12 +339,15 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   TT ker;
   CrossInfo ci;
   CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, nullptr, 0), S.xs, ker, &ci, S.sm));
-  if (c.leader()) put_cross(&dg->cross[1], ci);
+  if (c.leader()) { put_cross(&dg->cross[1], ci); log_ranks(dg, 4, ker); dg->cycles[4] = clk() - t0; }
+  t0 = clk();
   CK(tt_compact(c, ar, m1, ker));
   // FFT convolution + rounding
   TT conv;
   CK(tt_fft_conv(c, ar, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, conv, S.sm));
   CK(tt_compact(c, ar, m0, conv));
+  if (c.leader()) { log_ranks(dg, 5, conv); dg->cycles[5] = clk() - t0; }
+  t0 = clk();
   int maxr = 1;
   for (int k = 0; k <= d; ++k) maxr = imax(maxr, conv.r[k]);
   if (maxr > 512) return E_ARG;
@@ -337,10 +363,12 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   const size_t m2 = ar.mark();
   TT rl;
   CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, seeds, nseeds), S.xs, rl, &ci, S.sm));
-  if (c.leader()) put_cross(&dg->cross[2], ci);
+  if (c.leader()) { put_cross(&dg->cross[2], ci); log_ranks(dg, 6, rl); dg->cycles[6] = clk() - t0; }
+  t0 = clk();
   CK(tt_compact(c, ar, m2, rl));
   CK(finalize_tt(c, ar, rl, gcfg, spd, probes, nprobes, dg, S.sm));
   CK(tt_store(c, rl, hdr, state, cap));
+  if (c.leader()) { log_ranks(dg, 7, rl); dg->cycles[7] = clk() - t0; }
   return OK;
 }
 
