@@ -118,6 +118,11 @@ typedef struct {
    * 1 Hadamard+finalize, 2 moments, 3 interp+finalize, 4 kernel cross,
    * 5 FFT conv+round, 6 realign cross, 7 final finalize */
   int64_t cycles[8];
+  /* engine profile (SM cycles, CTA leader, overlapping categories):
+   * 0 miss sort, 1 evaluator, 2 cache lookup/insert, 3 core lstsq, 4 hunt,
+   * 5 accept, 6 cache check, 7 tt_round, 8 svd, 9 qr, 10 rng choice,
+   * 11 snapshot, 12 chain eval, 13 inject, 14 fft conv body, 15 negative mass */
+  int64_t prof[16];
 } ttgbf_diag;
 
 /* Model constants (StateSpaceModel, models.py:85-153).  Matrices row-major
@@ -139,6 +144,7 @@ typedef struct {
   double Lr[TTGBF_MAXB * TTGBF_MAXB];
   double logn_r;
   double H[TTGBF_MAXB * TTGBF_MAXD];
+  double Q[TTGBF_MAXD * TTGBF_MAXD];
 } ttgbf_model;
 
 /* Gaussian prior (initial_pmd_tt) */
@@ -158,6 +164,41 @@ typedef struct {
   int32_t has_z;
   int32_t active;
 } ttgbf_filter_io;
+
+/* Persistent multi-step run (device geometry): per-filter loop of
+ * tt_fft_pmf_step over `steps` steps, re-initialising from the prior on
+ * DegenerateDensityError and after kf steps (end of the trajectory). */
+typedef struct {
+  int32_t n_per_axis;
+  int32_t kf;             /* trajectory length (measurements per filter) */
+  int32_t steps;          /* filter steps attempted per filter in this launch */
+  int32_t pad;
+  double sigma_mult;
+  ttgbf_axis prior_grid[TTGBF_MAXD];
+} ttgbf_run_cfg;
+
+/* one record per filter per attempted step */
+typedef struct {
+  int32_t status;         /* 0 = step completed, else TTGBF_E_*; -1 = prior init failed */
+  int32_t k;              /* trajectory index of the measurement used */
+  int32_t spd_fixed;
+  int32_t outlier;
+  double mean[TTGBF_MAXD];
+  double cov_diag[TTGBF_MAXD];
+  double mass_before_norm;
+  double clipped_mass;
+  int64_t calls[3];
+  int32_t ranks[8][TTGBF_MAXD + 1];
+} ttgbf_step_rec;
+
+/* io[f].active is the filter's alive flag and io[f].cur its grid (in/out);
+ * kstep[f] its trajectory position (in/out); Z: nfilt x kf x b measurements;
+ * rec: nfilt x steps records. */
+int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
+                     ttgbf_run_cfg rcfg, ttgbf_filter_io* io, int32_t* kstep, const double* Z, int nfilt,
+                     const int32_t* probes, int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr,
+                     double* state, int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag,
+                     ttgbf_step_rec* rec, void* stream);
 
 /* ---- filter stages: one CTA per filter, nfilt filters per launch ---------
  * state_hdr[f] / state + f*state_cap: the filter's TT weights (in/out).

@@ -32,12 +32,17 @@ CROSS_INFO = np.dtype([("achieved", "f8"), ("calls", "i8"), ("sweeps", "i4"), ("
                       align=True)
 DIAG = np.dtype([("status", "i4"), ("outlier", "i4"), ("mass_before_norm", "f8"),
                  ("clipped_mass", "f8"), ("cross", CROSS_INFO, 3), ("raw_moments", "f8", NMOM),
-                 ("ws_peak", "i8"), ("ranks", "i4", (8, MAXD + 1)), ("cycles", "i8", 8)], align=True)
+                 ("ws_peak", "i8"), ("ranks", "i4", (8, MAXD + 1)), ("cycles", "i8", 8),
+                 ("prof", "i8", 16)], align=True)
 MODEL = np.dtype([("d", "i4"), ("b", "i4"), ("hkind", "i4"), ("nang", "i4"), ("ang", "i4", MAXB),
                   ("F", "f8", MAXD * MAXD), ("Finv", "f8", MAXD * MAXD), ("Lq", "f8", MAXD * MAXD),
                   ("logn_q", "f8"), ("Lr", "f8", MAXB * MAXB), ("logn_r", "f8"),
-                  ("H", "f8", MAXB * MAXD)], align=True)
+                  ("H", "f8", MAXB * MAXD), ("Q", "f8", MAXD * MAXD)], align=True)
 GAUSS = np.dtype([("mean", "f8", MAXD), ("L", "f8", MAXD * MAXD), ("logn", "f8")], align=True)
+RUN_CFG_FIELDS = None
+STEP_REC = np.dtype([("status", "i4"), ("k", "i4"), ("spd_fixed", "i4"), ("outlier", "i4"), ("mean", "f8", MAXD),
+                     ("cov_diag", "f8", MAXD), ("mass_before_norm", "f8"), ("clipped_mass", "f8"),
+                     ("calls", "i8", 3), ("ranks", "i4", (8, MAXD + 1))], align=True)
 FILTER_IO = np.dtype([("cur", AXIS, MAXD), ("filt", AXIS, MAXD), ("pred", AXIS, MAXD),
                       ("z", "f8", MAXB), ("has_z", "i4"), ("active", "i4")], align=True)
 
@@ -45,6 +50,16 @@ FILTER_IO = np.dtype([("cur", AXIS, MAXD), ("filt", AXIS, MAXD), ("pred", AXIS, 
 class GridCfg(ctypes.Structure):
     _fields_ = [("round_tol", ctypes.c_double), ("round_max_rank", ctypes.c_int32),
                 ("normalize_before_round", ctypes.c_int32), ("densify_guard", ctypes.c_int64)]
+
+
+class Axis(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_double), ("step", ctypes.c_double), ("off", ctypes.c_int32),
+                ("n", ctypes.c_int32)]
+
+
+class RunCfg(ctypes.Structure):
+    _fields_ = [("n_per_axis", ctypes.c_int32), ("kf", ctypes.c_int32), ("steps", ctypes.c_int32),
+                ("pad", ctypes.c_int32), ("sigma_mult", ctypes.c_double), ("prior_grid", Axis * MAXD)]
 
 
 class CrossCfg(ctypes.Structure):
@@ -63,6 +78,7 @@ SIGNATURES = {
     "ttgbf_filter_prior": [P, P, GridCfg, CrossCfg, P, I32, P, I32, P, P, I64, P, I64, P, P],
     "ttgbf_filter_measure": [P, GridCfg, CrossCfg, P, I32, P, I32, P, I32, P, P, I64, P, I64, P, P],
     "ttgbf_filter_time_update": [P, GridCfg, CrossCfg, P, I32, P, I32, P, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_filter_run": [P, P, GridCfg, CrossCfg, RunCfg, P, P, P, I32, P, I32, P, I32, P, P, I64, P, I64, P, P, P],
     "ttgbf_tt_round": [P, P, I64, I32, F64, I32, P, P, I64, P, I64, P, P],
     "ttgbf_tt_hadamard": [P, P, I64, P, P, I64, I32, P, P, I64, P, I64, P, P],
     "ttgbf_tt_fft_convolve": [P, P, I64, P, P, I64, I32, F64, I32, P, P, I64, P, I64, P, P],

@@ -90,6 +90,7 @@ def model_record(spec) -> np.ndarray:
         rec[field][0] = buf
 
     put("F", F, _abi.MAXD)
+    put("Q", Q, _abi.MAXD)
     try:
         Finv = np.linalg.inv(F)
     except np.linalg.LinAlgError:
@@ -289,6 +290,51 @@ class FilterBank:
                 means[i], covs[i] = geom[i][1][0], geom[i][1][1]
         self.alive &= status == 0
         return {"status": status, "mean": means, "cov": covs, "measure": dm, "time": dt, "geom": geom}
+
+    # -- persistent multi-step run (device geometry) ----------------------------
+    def run(self, Z, steps, prior_mean, prior_cov):
+        """``steps`` tt_fft_pmf_step calls per filter in ONE kernel launch.
+
+        Z: (count, kf, b) measurements (each filter replays its trajectory from
+        k=0 after a restart).  Dead filters (re)start from the prior on the
+        device.  Returns the (count, steps) STEP_REC records.
+        """
+        Z = np.ascontiguousarray(np.asarray(Z, dtype=float))
+        kf = Z.shape[1]
+        if not hasattr(self, "_run_prior") or self._run_prior[0] is not prior_mean:
+            grid = geo.design_grid(prior_mean, prior_cov, self.cfg.n_per_axis, self.cfg.sigma_mult)
+            self._run_prior = (prior_mean, self.be.upload(gauss_record(prior_mean, prior_cov)), grid)
+            self.kstep_dev = self.be.upload(np.zeros(self.count, dtype=np.int32))
+        _, prior_dev, grid = self._run_prior
+        rc = _abi.RunCfg()
+        rc.n_per_axis = int(self.cfg.n_per_axis)
+        rc.kf = int(kf)
+        rc.steps = int(steps)
+        rc.sigma_mult = float(self.cfg.sigma_mult)
+        dev = grid.device()
+        for k in range(_abi.MAXD):
+            rc.prior_grid[k].base = float(dev["base"][k])
+            rc.prior_grid[k].step = float(dev["step"][k])
+            rc.prior_grid[k].off = int(dev["off"][k])
+            rc.prior_grid[k].n = int(dev["n"][k])
+        zb = self.be.upload(Z)
+        self.bytes_h2d += Z.nbytes
+        rec = self.be.empty(self.count * max(1, steps) * _abi.STEP_REC.itemsize)
+        self.io["active"] = self.alive.astype(np.int32)
+        self._push_io()
+        pr, npr, sd, nsd = self._ptrs()
+        self._launch("ttgbf_filter_run", self.lib.ttgbf_filter_run, self.model.ptr, prior_dev.ptr, self.gcfg,
+                     self.xcfg, rc, self.io_dev.ptr, self.kstep_dev.ptr, zb.ptr, self.count, pr, npr, sd, nsd,
+                     self.hdr.ptr, self.state.ptr, self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes,
+                     self.diag_dev.ptr, rec.ptr, self.be.stream_ptr)
+        recs = self.be.download(rec, _abi.STEP_REC, self.count * steps).reshape(self.count, steps)
+        self.io = self.be.download(self.io_dev, _abi.FILTER_IO, self.count)
+        self.bytes_d2h += recs.nbytes + self.io.nbytes
+        self.alive = self.io["active"].astype(bool)
+        for i in range(self.count):
+            c = self.io["cur"][i]
+            self.grids[i] = geo.Axes(c["base"][: self.d], c["step"][: self.d], c["off"][: self.d], c["n"][: self.d])
+        return recs
 
     # -- state access -----------------------------------------------------------
     def headers(self) -> np.ndarray:

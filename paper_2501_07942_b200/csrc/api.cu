@@ -22,7 +22,7 @@ namespace {
 
 #ifdef __CUDACC__
 template <class F>
-__global__ void __launch_bounds__(BLOCK_THREADS) k_items(F f, int count) {
+__global__ void __launch_bounds__(BLOCK_THREADS, 2) k_items(F f, int count) {
   extern __shared__ double smem[];
   const Ctx c = make_ctx(smem, threadIdx.x, blockDim.x);
   if ((int)blockIdx.x < count) f(c, (int)blockIdx.x, smem);
@@ -95,11 +95,17 @@ int ttgbf_filter_measure(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cr
                          const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
                          const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr, double* state,
                          int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag, void* stream) {
-  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+  auto f = LAMBDA(const Ctx& c0, int i, double* smem) {
     if (!io[i].active) return;
     Arena ar = make_arena(ws, ws_bytes, i);
     ttgbf_diag* dg = diag + i;
-    if (c.leader()) { dg->clipped_mass = 0.0; dg->outlier = 0; dg->mass_before_norm = NAN; }
+    Ctx c = c0;
+    c.prof = dg->prof;
+    if (c.leader()) {
+      dg->clipped_mass = 0.0; dg->outlier = 0; dg->mass_before_norm = NAN;
+      for (int q = 0; q < 16; ++q) dg->prof[q] = 0;
+      for (int q = 0; q < 8; ++q) dg->cycles[q] = 0;
+    }
     c.sync();
     int st = stage_measure(c, ar, *model, gcfg, xcfg, io[i], probes, nprobes, seeds, nseeds, state_hdr + i,
                            state + (int64_t)i * state_cap, state_cap, dg, make_stage_smem(smem));
@@ -112,16 +118,43 @@ int ttgbf_filter_time_update(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgb
                              const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
                              const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr, double* state,
                              int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag, void* stream) {
-  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+  auto f = LAMBDA(const Ctx& c0, int i, double* smem) {
     if (!io[i].active) return;
     Arena ar = make_arena(ws, ws_bytes, i);
     ttgbf_diag* dg = diag + i;
+    Ctx c = c0;
+    c.prof = dg->prof;
     int st = stage_time(c, ar, *model, gcfg, xcfg, io[i], probes, nprobes, seeds, nseeds, state_hdr + i,
                         state + (int64_t)i * state_cap, state_cap, dg, make_stage_smem(smem));
     if (c.leader()) {
       dg->status = st;
       if ((int64_t)ar.peak > dg->ws_peak) dg->ws_peak = (int64_t)ar.peak;
     }
+  };
+  return launch(nfilt, f, stream);
+}
+
+int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
+                     ttgbf_run_cfg rcfg, ttgbf_filter_io* io, int32_t* kstep, const double* Z, int nfilt,
+                     const int32_t* probes, int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr,
+                     double* state, int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag,
+                     ttgbf_step_rec* rec, void* stream) {
+  if (rcfg.steps < 0 || rcfg.kf < 1) return TTGBF_E_ARG;
+  auto f = LAMBDA(const Ctx& c0, int i, double* smem) {
+    Arena ar = make_arena(ws, ws_bytes, i);
+    ttgbf_diag* dg = diag + i;
+    Ctx c = c0;
+    c.prof = dg->prof;
+    if (c.leader()) {
+      for (int q = 0; q < 16; ++q) dg->prof[q] = 0;
+      for (int q = 0; q < 8; ++q) dg->cycles[q] = 0;
+    }
+    c.sync();
+    const int b = model->b;
+    int st = stage_run(c, ar, *model, *prior, gcfg, xcfg, rcfg, io + i, kstep + i, Z + (int64_t)i * rcfg.kf * b,
+                       probes, nprobes, seeds, nseeds, state_hdr + i, state + (int64_t)i * state_cap, state_cap, dg,
+                       rec + (int64_t)i * rcfg.steps, make_stage_smem(smem));
+    if (c.leader()) { dg->status = st; dg->ws_peak = (int64_t)ar.peak; }
   };
   return launch(nfilt, f, stream);
 }
@@ -245,3 +278,64 @@ int ttgbf_negative_mass(const ttgbf_tt* hdr, const double* data, int64_t cap, in
 }
 
 }  // extern "C"
+
+#ifdef ENGINE_HOSTSIM
+// Test-only hooks (host emulation build): numpy-stream draws through the
+// same warp-parallel code the device cross uses.
+extern "C" int ttgbf_test_draws(int kind, uint64_t* state6, const int* shape, int d, int64_t K, int64_t pop,
+                                int64_t size, int64_t* out) {
+  std::vector<double> smem(SMEM_DOUBLES);
+  const Ctx c = make_ctx(smem.data(), 0, 1);
+  Pcg64 g;
+  g.s_lo = state6[0]; g.s_hi = state6[1]; g.i_lo = state6[2]; g.i_hi = state6[3];
+  g.has32 = (uint32_t)state6[4]; g.u32 = (uint32_t)state6[5];
+  PcgJump jt;
+  pcg_make_jump(g, &jt);
+  DrawBuf db;
+  if (kind == 0) {
+    std::vector<int64_t> tmp(K * d);
+    std::vector<int32_t> o32(K * d);
+    warp_integers(c, &g, &jt, shape, d, K, o32.data(), tmp.data(), &db);
+    for (int64_t e = 0; e < K * d; ++e) out[e] = o32[e];
+  } else {
+    std::vector<int32_t> disp(pop + 16, -1);
+    std::vector<int64_t> touch(size + 16), draws(size + 16);
+    std::vector<uint64_t> gset(2 * (size + 16) + 64);
+    warp_choice(c, &g, &jt, pop, size, out, disp.data(), touch.data(), draws.data(),
+                reinterpret_cast<uint32_t*>(smem.data() + SMEM_RED + SMEM_XBLK), 16384, gset.data(), &db);
+    for (int64_t q = 0; q < pop; ++q)
+      if (disp[q] != -1) return 99;   // displacement map must be restored
+  }
+  state6[0] = g.s_lo; state6[1] = g.s_hi; state6[2] = g.i_lo; state6[3] = g.i_hi;
+  state6[4] = g.has32; state6[5] = g.u32;
+  return 0;
+}
+#endif
+
+#ifdef ENGINE_HOSTSIM
+// Test-only: blocked QR of A (m x n col-major, overwritten) and Q (m x k) = Q [I; 0].
+extern "C" int ttgbf_test_qr(double* A, int m, int n, double* Q, void* ws, int64_t ws_bytes) {
+  std::vector<double> smem(SMEM_DOUBLES);
+  const Ctx c = make_ctx(smem.data(), 0, 1);
+  Arena ar = make_arena(ws, ws_bytes, 0);
+  const int k = m < n ? m : n;
+  std::vector<double> tau(k), Ts(((k + NB - 1) / NB) * NB * NB);
+  int st = geqrf_nb(c, ar, A, m, m, n, tau.data(), Ts.data(), smem.data() + SMEM_RED + SMEM_XBLK);
+  if (st) return st;
+  for (int64_t e = 0; e < (int64_t)m * k; ++e) Q[e] = ((e % m) == (e / m)) ? 1.0 : 0.0;
+  return apply_q(c, ar, A, m, m, k, Ts.data(), false, Q, m, k, smem.data() + SMEM_RED + SMEM_XBLK);
+}
+#endif
+
+#ifdef ENGINE_HOSTSIM
+extern "C" int ttgbf_test_qr_apply(double* A, int m, int n, double* X, int nc, void* ws, int64_t ws_bytes) {
+  std::vector<double> smem(SMEM_DOUBLES);
+  const Ctx c = make_ctx(smem.data(), 0, 1);
+  Arena ar = make_arena(ws, ws_bytes, 0);
+  const int k = m < n ? m : n;
+  std::vector<double> tau(k), Ts(((k + NB - 1) / NB) * NB * NB);
+  int st = geqrf_nb(c, ar, A, m, m, n, tau.data(), Ts.data(), smem.data() + SMEM_RED + SMEM_XBLK);
+  if (st) return st;
+  return apply_q(c, ar, A, m, m, k, Ts.data(), false, X, m, nc, smem.data() + SMEM_RED + SMEM_XBLK);
+}
+#endif

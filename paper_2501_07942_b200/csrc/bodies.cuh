@@ -7,7 +7,7 @@
 namespace tg {
 
 constexpr int SMEM_RED = 64 + 1024;       // reductions + scan buffer (doubles)
-constexpr int SMEM_XBLK = 160;            // XShared + XState (doubles)
+constexpr int SMEM_XBLK = 576;            // XShared (+ draw buffer) + XState (doubles)
 constexpr int SMEM_SCRATCH = 8192;        // gemm tiles / QR / chain evaluation
 constexpr int SMEM_DOUBLES = SMEM_RED + SMEM_XBLK + SMEM_SCRATCH;
 constexpr int BLOCK_THREADS = 256;
@@ -20,6 +20,7 @@ HD Ctx make_ctx(double* smem, int tid, int nt) {
   c.nt = nt;
   c.red = smem;
   c.ired = reinterpret_cast<int*>(smem + 32);
+  c.prof = nullptr;
   return c;
 }
 HD StageSmem make_stage_smem(double* smem) {

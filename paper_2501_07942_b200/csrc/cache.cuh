@@ -158,9 +158,12 @@ HDN int64_t scan_offsets(const Ctx& c, int64_t mine, int64_t* total) {
 }
 
 // Evaluate K multi-indices (int32, K x d) through the cache; out[K].
+// presorted: idx is already in strictly ascending key order (no duplicates),
+// so the misses need no sort (Cartesian fibre blocks enumerated in order).
 HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, const int32_t* idx,
-                          int64_t K, double* out, double* sm) {
+                          int64_t K, double* out, double* sm, bool presorted = false) {
   const int d = C->d, bits = C->bits;
+  PROF(c, 2);
   size_t mk = ar.mark();
   int64_t* pos;
   ALLOC(pos, int64_t, K > 0 ? K : 1, ar);
@@ -182,14 +185,27 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
     if (pos[p] < 0) mkeys[off++] = pack_key(d, bits, idx + p * d);
   c.sync();
   if (total > 0) {
-    // 2. sort + dedup
+    // 2. sort + dedup (skipped for presorted blocks: compaction kept the order)
     int64_t P = 1;
     while (P < total) P <<= 1;
-    Key* sk;
-    ALLOC(sk, Key, P, ar);
-    for (int64_t i = c.tid; i < P; i += c.nt) sk[i] = (i < total) ? mkeys[i] : Key{~0ull, ~0ull};
-    c.sync();
-    bitonic_sort(c, sk, P);
+    Key* sk = mkeys;
+    if (!presorted) {
+      PROF(c, 0);
+      const bool in_smem = P * (int64_t)sizeof(Key) <= (int64_t)(8192 * sizeof(double));
+      if (in_smem) {
+        sk = reinterpret_cast<Key*>(sm);
+      } else {
+        ALLOC(sk, Key, P, ar);
+      }
+      for (int64_t i = c.tid; i < P; i += c.nt) sk[i] = (i < total) ? mkeys[i] : Key{~0ull, ~0ull};
+      c.sync();
+      bitonic_sort(c, sk, P);
+      if (in_smem) {   // move back to global: sm is reused by the evaluator
+        for (int64_t i = c.tid; i < total; i += c.nt) mkeys[i] = sk[i];
+        c.sync();
+        sk = mkeys;
+      }
+    }
     const int64_t ch2 = (total + c.nt - 1) / c.nt;
     const int64_t lo2 = lmin(total, (int64_t)c.tid * ch2), hi2 = lmin(total, lo2 + ch2);
     int64_t nu = 0;
@@ -211,6 +227,7 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
     for (int64_t j = c.tid; j < M; j += c.nt) unpack_key(d, bits, C->keys[base + j], uidx + j * d);
     c.sync();
     double* nv = C->vals + base;
+    PROF(c, 1);
     if (spec.kind == EV_REALIGN) {
       struct RPt {
         const EvalSpec* s;

@@ -50,6 +50,23 @@ enum Status : int {
 
 #define CK(expr) do { int _st = (expr); if (_st) return _st; } while (0)
 
+HD int64_t clk() {
+#if ENGINE_DEVICE
+  return (int64_t)clock64();
+#else
+  return 0;
+#endif
+}
+// profile scope: leader accumulates elapsed SM cycles into ctx.prof[cat]
+struct ProfScope {
+  const int64_t* dummy;
+  int64_t* slot;
+  int64_t t0;
+  HD ProfScope(int64_t* p, int tid, int cat) : dummy(nullptr), slot((p && tid == 0) ? p + cat : nullptr), t0(clk()) {}
+  HD ~ProfScope() { if (slot) *slot += clk() - t0; }
+};
+#define PROF(c, cat) ::tg::ProfScope _prof_##cat((c).prof, (c).tid, cat)
+
 HD int imin(int a, int b) { return a < b ? a : b; }
 HD int imax(int a, int b) { return a > b ? a : b; }
 HD int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }
@@ -63,6 +80,7 @@ struct Ctx {
   int nt;
   double* red;   // shared scratch, >= 64 doubles (+ 64 ints after it)
   int* ired;     // shared scratch, >= 64 ints
+  int64_t* prof; // optional per-CTA profile counters (leader), may be null
 
   HD void sync() const {
 #if ENGINE_DEVICE

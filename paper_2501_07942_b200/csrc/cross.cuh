@@ -8,6 +8,7 @@
 #pragma once
 #include "common.cuh"
 #include "rng.cuh"
+#include "rng_warp.cuh"
 #include "linalg.cuh"
 #include "tt.cuh"
 #include "models.cuh"
@@ -56,6 +57,15 @@ struct XShared {           // leader-published scalars
   Pcg64 rng;
   int64_t i0, i1, i2;
   double f0, f1;
+  DrawBuf db;              // warp-parallel draw buffer
+};
+
+struct ChoiceWs {
+  int32_t* disp;     // virtual arange for tail shuffles (-1 = untouched)
+  uint64_t* gset;    // Floyd set when it does not fit shared memory
+  int64_t* touch;    // touched positions / shuffle draws
+  int64_t* draws;    // pre-drawn bounded values
+  const PcgJump* jt; // PCG64 jump-ahead table of this stream
 };
 
 HD int x_left(const XState& s, int k) { return k == 0 ? 1 : s.rank[k]; }
@@ -66,21 +76,45 @@ HD int x_limit(const XState& s, int b, int max_rank) {
 HD const int16_t* x_lrow(const XState& s, int k, int a) { return k == 0 ? nullptr : s.rows[k] + a * MAXD; }
 HD const int16_t* x_rcol(const XState& s, int k, int c) { return k == s.d - 1 ? nullptr : s.cols[k + 1] + c * MAXD; }
 
-// Cartesian block (left(k) x arange(n_k) x right(k)) restricted to the
-// left rows [a0, a1) and right cols [c0, c1): index array, suffix fastest.
-HDN void x_block_idx(const Ctx& c, const XState& s, int k, int a0, int a1, int c0, int c1, int32_t* idx) {
+HD bool tuple_lt(const int16_t* a, const int16_t* b, int len) {
+  for (int j = 0; j < len; ++j)
+    if (a[j] != b[j]) return a[j] < b[j];
+  return false;
+}
+
+// leader: order[0..cnt) = indices of list rows [base, base+cnt) sorted by tuple
+HD void sort_tuples(const int16_t* list, int base, int cnt, int len, int* order) {
+  for (int t = 0; t < cnt; ++t) order[t] = base + t;
+  for (int t = 1; t < cnt; ++t) {
+    int p = order[t], q = t - 1;
+    while (q >= 0 && tuple_lt(list + p * MAXD, list + order[q] * MAXD, len)) { order[q + 1] = order[q]; --q; }
+    order[q + 1] = p;
+  }
+}
+
+// Cartesian block (left(k) x arange(n_k) x right(k)) restricted to the left
+// rows [a0, a1) and right cols [c0, c1), enumerated in ascending key order
+// (sorted prefixes, mode index, sorted suffixes).  lo[] / co[] receive the
+// original row / col of each sorted position.
+HDN void x_block_idx(const Ctx& c, const XState& s, int k, int a0, int a1, int c0, int c1, int32_t* idx,
+                     int* lo, int* co) {
   const int d = s.d, n = s.n[k];
   const int na = a1 - a0, nc = c1 - c0;
+  if (c.leader()) {
+    if (k == 0) lo[0] = 0; else sort_tuples(s.rows[k], a0, na, k, lo);
+    if (k == d - 1) co[0] = 0; else sort_tuples(s.cols[k + 1], c0, nc, d - k - 1, co);
+  }
+  c.sync();
   const int64_t tot = (int64_t)na * n * nc;
   for (int64_t e = c.tid; e < tot; e += c.nt) {
     const int cc = (int)(e % nc);
     const int i = (int)((e / nc) % n);
     const int aa = (int)(e / ((int64_t)nc * n));
     int32_t* o = idx + e * d;
-    const int16_t* L = x_lrow(s, k, a0 + aa);
+    const int16_t* L = x_lrow(s, k, lo[aa]);
     for (int j = 0; j < k; ++j) o[j] = L[j];
     o[k] = i;
-    const int16_t* R = x_rcol(s, k, c0 + cc);
+    const int16_t* R = x_rcol(s, k, co[cc]);
     for (int j = 0; j < d - k - 1; ++j) o[k + 1 + j] = R[j];
   }
   c.sync();
@@ -95,16 +129,19 @@ HDN int x_fill_fib(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XSta
   size_t mk = ar.mark();
   int32_t* idx;
   double* v;
+  int *lo, *co;
   ALLOC(idx, int32_t, tot * s.d, ar);
   ALLOC(v, double, tot, ar);
-  x_block_idx(c, s, k, a0, a1, c0, c1, idx);
-  CK(cache_eval(c, ar, C, spec, idx, tot, v, sm));
+  ALLOC(lo, int, a1 - a0, ar);
+  ALLOC(co, int, c1 - c0, ar);
+  x_block_idx(c, s, k, a0, a1, c0, c1, idx, lo, co);
+  CK(cache_eval(c, ar, C, spec, idx, tot, v, sm, true));
   const int nc = c1 - c0;
   for (int64_t e = c.tid; e < tot; e += c.nt) {
     const int cc = (int)(e % nc);
     const int i = (int)((e / nc) % n);
     const int aa = (int)(e / ((int64_t)nc * n));
-    s.fib[k][((int64_t)(a0 + aa) * n + i) * s.ccap[k] + c0 + cc] = v[e];
+    s.fib[k][((int64_t)lo[aa] * n + i) * s.ccap[k] + co[cc]] = v[e];
   }
   c.sync();
   ar.release(mk);
@@ -152,6 +189,7 @@ HDN int x_solve_core(const Ctx& c, Arena& ar, XState& s, int k) {
     c.sync();
     return OK;
   }
+  PROF(c, 3);
   size_t mk = ar.mark();
   const int r = Cc;
   double *W, *W2, *tau, *tau2, *cn;
@@ -171,6 +209,7 @@ HDN int x_solve_core(const Ctx& c, Arena& ar, XState& s, int k) {
 
 // compact snapshot of the current interpolant
 HDN int x_snapshot(const Ctx& c, Arena& ar, const XState& s, TT& t) {
+  PROF(c, 11);
   int r[MAXD + 1];
   r[0] = 1;
   for (int b = 1; b < s.d; ++b) r[b] = s.rank[b];
@@ -204,6 +243,7 @@ HD bool tuple_in(const int16_t* list, int cnt, const int16_t* x, int len) {
 // already appended to s.rows[b]/s.cols[b] at positions [old, old+m).
 HDN int x_accept(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& s, int b, int m,
                         double* sm) {
+  PROF(c, 5);
   const int old = s.rank[b];
   // row block (new rows x old cols), then col block (all rows x new cols)
   CK(x_fill_ahat(c, ar, C, spec, s, b, old, old + m, 0, old, sm));
@@ -264,7 +304,8 @@ struct Cand {
 // _hunt_candidates (tt_algorithms.py:341-421).  Writes up to 101 candidates
 // (rook winner first) to `cand`, returns count and err_seen.
 HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& s, int b, XShared* sh,
-                      uint64_t* rws, Cand* cand, int* ncand, double* err_seen, double* sm) {
+                      const ChoiceWs& rws, Cand* cand, int* ncand, double* err_seen, double* sm) {
+  PROF(c, 4);
   HuntGeo g;
   g.b = b;
   g.nl = s.n[b - 1];
@@ -281,9 +322,12 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
   ALLOC(br, int64_t, X_SCAN, ar);
   ALLOC(bc, int64_t, X_SCAN, ar);
   ALLOC(e, double, X_SCAN, ar);
+  {
+    PROF(c, 10);
+    warp_choice(c, &sh->rng, rws.jt, g.nrow, qr, cr, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, g.ncol, qc, cc, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+  }
   if (c.leader()) {
-    pcg_choice(sh->rng, g.nrow, qr, cr, rws);
-    pcg_choice(sh->rng, g.ncol, qc, cc, rws);
     for (int i = 0; i < qr; ++i)
       for (int j = 0; j < qc; ++j) { br[i * qc + j] = cr[i]; bc[i * qc + j] = cc[j]; }
   }
@@ -316,8 +360,12 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
   for (int it = 0; it < X_ROOK; ++it) {
     // column scan over (sampled) rows
     int nsr = 0;
+    if (g.nrow > X_SCAN) {
+      PROF(c, 10);
+      warp_choice(c, &sh->rng, rws.jt, g.nrow, X_SCAN, br, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+    }
     if (c.leader()) {
-      if (g.nrow > X_SCAN) { pcg_choice(sh->rng, g.nrow, X_SCAN, br, rws); nsr = X_SCAN; }
+      if (g.nrow > X_SCAN) nsr = X_SCAN;
       else { for (int i = 0; i < g.nrow; ++i) br[i] = i; nsr = g.nrow; }
       for (int i = 0; i < nsr; ++i) bc[i] = cbest;
       sh->i2 = nsr;
@@ -332,8 +380,12 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
     const double mcol = best.v;
     c.sync();
     int nsc = 0;
+    if (g.ncol > X_SCAN) {
+      PROF(c, 10);
+      warp_choice(c, &sh->rng, rws.jt, g.ncol, X_SCAN, bc, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+    }
     if (c.leader()) {
-      if (g.ncol > X_SCAN) { pcg_choice(sh->rng, g.ncol, X_SCAN, bc, rws); nsc = X_SCAN; }
+      if (g.ncol > X_SCAN) nsc = X_SCAN;
       else { for (int i = 0; i < g.ncol; ++i) bc[i] = i; nsc = g.ncol; }
       for (int i = 0; i < nsc; ++i) br[i] = rnew;
       sh->i2 = nsc;
@@ -376,9 +428,10 @@ HD void x_split(const XState& s, int b, int64_t row, int64_t col, int16_t* rt, i
 
 // _cache_check (tt_algorithms.py:424-433): worst `top` errors over a random
 // cache subsample; out_err/out_cell (cells as int32 x d), sorted worst first.
-HDN int x_check(const Ctx& c, Arena& ar, Cache* C, XShared* sh, uint64_t* rws, const TT& t,
+HDN int x_check(const Ctx& c, Arena& ar, Cache* C, XShared* sh, const ChoiceWs& rws, const TT& t,
                        int count, int top, double* out_err, int32_t* out_cell, int* nout, double* sm) {
   const int d = C->d;
+  PROF(c, 6);
   size_t mk = ar.mark();
   const int64_t cnt = C->count;
   const int64_t K = cnt > count ? count : cnt;
@@ -389,9 +442,11 @@ HDN int x_check(const Ctx& c, Arena& ar, Cache* C, XShared* sh, uint64_t* rws, c
   ALLOC(idx, int32_t, K * d, ar);
   ALLOC(vals, double, K, ar);
   ALLOC(tv, double, K, ar);
-  if (c.leader()) {
-    if (cnt > count) pcg_choice(sh->rng, cnt, count, sel, rws);
-    else for (int64_t i = 0; i < cnt; ++i) sel[i] = i;
+  if (cnt > count) {
+    PROF(c, 10);
+    warp_choice(c, &sh->rng, rws.jt, cnt, count, sel, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+  } else if (c.leader()) {
+    for (int64_t i = 0; i < cnt; ++i) sel[i] = i;
   }
   c.sync();
   for (int64_t p = c.tid; p < K; p += c.nt) {
@@ -399,7 +454,7 @@ HDN int x_check(const Ctx& c, Arena& ar, Cache* C, XShared* sh, uint64_t* rws, c
     vals[p] = C->vals[sel[p]];
   }
   c.sync();
-  tt_eval_idx(c, t, idx, K, tv, sm);
+  { PROF(c, 12); tt_eval_idx(c, t, idx, K, tv, sm); }
   for (int64_t p = c.tid; p < K; p += c.nt) tv[p] = fabs(vals[p] - tv[p]);
   c.sync();
   // top-k: repeated arg-max preferring the LAST index on ties (argsort[::-1])
@@ -431,6 +486,7 @@ HDN int x_inject(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState
                         const double* oerr, const int32_t* ocell, int nof, double thr, int max_rank,
                         bool* grew, double* sm) {
   const int d = s.d;
+  PROF(c, 13);
   int pend[MAXD];
   for (int b = 0; b < d; ++b) pend[b] = 0;
   // leader decides; pending rows/cols are appended to the state's lists
@@ -485,8 +541,22 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
   if (c.leader()) sh->rng = cfg.rng;
   c.sync();
   // RNG workspace for choice(): up to the gate sample from a large cache
-  uint64_t* rws;
-  ALLOC(rws, uint64_t, choice_ws_words(cfg.cache_cap + X_GATE + 16, X_GATE), ar);
+  ChoiceWs rws;
+  {
+    int maxn = 1;
+    for (int k = 0; k < d; ++k) maxn = imax(maxn, spec.n[k]);
+    const int64_t dcap = lmax(cfg.cache_cap + 16, (int64_t)cfg.max_rank * maxn + 16);
+    ALLOC(rws.gset, uint64_t, gen_mask((uint64_t)(1.2 * X_GATE)) + 1, ar);
+    ALLOC(rws.disp, int32_t, dcap, ar);
+    ALLOC(rws.touch, int64_t, X_GATE + X_SCAN, ar);
+    ALLOC(rws.draws, int64_t, X_GATE + X_SCAN, ar);
+    PcgJump* jt;
+    ALLOC(jt, PcgJump, 1, ar);
+    if (c.leader()) pcg_make_jump(cfg.rng, jt);
+    rws.jt = jt;
+    for (int64_t q = c.tid; q < dcap; q += c.nt) rws.disp[q] = -1;
+    c.sync();
+  }
   if (d == 1) {
     int32_t* idx;
     double* v;
@@ -509,7 +579,7 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
   double* pv;
   ALLOC(probes, int32_t, K0 * d, ar);
   ALLOC(pv, double, K0, ar);
-  if (c.leader()) pcg_integers(sh->rng, spec.n, d, nprobe, probes);
+  warp_integers(c, &sh->rng, rws.jt, spec.n, d, nprobe, probes, rws.draws, &sh->db);
   for (int64_t e = c.tid; e < (int64_t)cfg.nseeds * d; e += c.nt) probes[(int64_t)nprobe * d + e] = cfg.seeds[e];
   c.sync();
   CK(cache_eval(c, ar, C, spec, probes, K0, pv, sm));
@@ -638,7 +708,7 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
       }
     }
     // fresh uniform probes
-    if (c.leader()) pcg_integers(sh->rng, spec.n, d, fresh, fp);
+    warp_integers(c, &sh->rng, rws.jt, spec.n, d, fresh, fp, rws.draws, &sh->db);
     c.sync();
     CK(cache_eval(c, ar, C, spec, fp, fresh, fv, sm));
     double thr = cfg.tol * fmax(C->max_abs, X_TINY);
@@ -696,7 +766,8 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
   ALLOC(vp, int32_t, (int64_t)nv * d, ar);
   ALLOC(vref, double, nv, ar);
   ALLOC(vt, double, nv, ar);
-  if (c.leader()) pcg_integers(sh->rng, spec.n, d, nv, vp);
+  if ((int64_t)nv * d > X_GATE + X_SCAN) return E_ARG;
+  warp_integers(c, &sh->rng, rws.jt, spec.n, d, nv, vp, rws.draws, &sh->db);
   c.sync();
   CK(cache_eval(c, ar, C, spec, vp, nv, vref, sm));
   auto validate = [&](const TT& cand_tt, double* res) -> int {

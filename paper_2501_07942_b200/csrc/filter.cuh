@@ -13,19 +13,13 @@
 #include "tt.cuh"
 #include "models.cuh"
 #include "cross.cuh"
+#include "geom.cuh"
 #include "../../include/ttgbf.h"
 
 namespace tg {
 
 constexpr double MASS_FLOOR = 1e-300;   // filters.py:100
 
-HD int64_t clk() {
-#if ENGINE_DEVICE
-  return (int64_t)clock64();
-#else
-  return 0;
-#endif
-}
 
 HD void log_ranks(ttgbf_diag* dg, int slot, const TT& t) {
   for (int k = 0; k <= TTGBF_MAXD; ++k) dg->ranks[slot][k] = k <= t.d ? t.r[k] : 0;
@@ -270,7 +264,7 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
     if (c.leader()) { put_cross(&dg->cross[0], ci); log_ranks(dg, 1, lik); }
     CK(tt_compact(c, ar, mk, lik));
     const int64_t t1 = clk();
-    if (c.leader()) dg->cycles[0] = t1 - t0;
+    if (c.leader()) dg->cycles[0] += t1 - t0;
     t0 = t1;
     const size_t mk2 = ar.mark();
     TT prod;
@@ -288,7 +282,7 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
       p = tt_view(hdr, state);
     }
   }
-  if (c.leader()) { log_ranks(dg, 2, p); dg->cycles[1] = clk() - t0; }
+  if (c.leader()) { log_ranks(dg, 2, p); dg->cycles[1] += clk() - t0; }
   t0 = clk();
   // raw moments of the filtering density
   const double* ax[MAXD];
@@ -298,7 +292,7 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
   CK(tt_moments(c, ar, p, ax, mom));
   const int nmom = 1 + d + d * (d + 1) / 2;
   for (int q = c.tid; q < nmom; q += c.nt) dg->raw_moments[q] = mom[q];
-  if (c.leader()) dg->cycles[2] = clk() - t0;
+  if (c.leader()) dg->cycles[2] += clk() - t0;
   c.sync();
   return OK;
 }
@@ -330,7 +324,7 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
     CK(tt_interp(c, ar, filt, gc, na, shifted));
   }
   CK(finalize_tt(c, ar, shifted, gcfg, sf, probes, nprobes, dg, S.sm));
-  if (c.leader()) { log_ranks(dg, 3, shifted); dg->cycles[3] = clk() - t0; }
+  if (c.leader()) { log_ranks(dg, 3, shifted); dg->cycles[3] += clk() - t0; }
   t0 = clk();
   // kernel cross on the filtering grid
   if (c.leader()) { spec_grid(*sp, d, af, io.filt); spec_kernel(*sp, model, sf); }
@@ -339,14 +333,14 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   TT ker;
   CrossInfo ci;
   CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, nullptr, 0), S.xs, ker, &ci, S.sm));
-  if (c.leader()) { put_cross(&dg->cross[1], ci); log_ranks(dg, 4, ker); dg->cycles[4] = clk() - t0; }
+  if (c.leader()) { put_cross(&dg->cross[1], ci); log_ranks(dg, 4, ker); dg->cycles[4] += clk() - t0; }
   t0 = clk();
   CK(tt_compact(c, ar, m1, ker));
   // FFT convolution + rounding
   TT conv;
   CK(tt_fft_conv(c, ar, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, conv, S.sm));
   CK(tt_compact(c, ar, m0, conv));
-  if (c.leader()) { log_ranks(dg, 5, conv); dg->cycles[5] = clk() - t0; }
+  if (c.leader()) { log_ranks(dg, 5, conv); dg->cycles[5] += clk() - t0; }
   t0 = clk();
   int maxr = 1;
   for (int k = 0; k <= d; ++k) maxr = imax(maxr, conv.r[k]);
@@ -363,12 +357,103 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   const size_t m2 = ar.mark();
   TT rl;
   CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, seeds, nseeds), S.xs, rl, &ci, S.sm));
-  if (c.leader()) { put_cross(&dg->cross[2], ci); log_ranks(dg, 6, rl); dg->cycles[6] = clk() - t0; }
+  if (c.leader()) { put_cross(&dg->cross[2], ci); log_ranks(dg, 6, rl); dg->cycles[6] += clk() - t0; }
   t0 = clk();
   CK(tt_compact(c, ar, m2, rl));
   CK(finalize_tt(c, ar, rl, gcfg, spd, probes, nprobes, dg, S.sm));
   CK(tt_store(c, rl, hdr, state, cap));
-  if (c.leader()) { log_ranks(dg, 7, rl); dg->cycles[7] = clk() - t0; }
+  if (c.leader()) { log_ranks(dg, 7, rl); dg->cycles[7] += clk() - t0; }
+  return OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// Persistent multi-step run: this filter's loop over rc.steps tt_fft_pmf_step
+// calls with device geometry, restarting from the prior after a failure or
+// at the end of its trajectory (bench / Monte Carlo driver).
+// ---------------------------------------------------------------------------
+HDN int stage_run(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_gauss& prior,
+                  const ttgbf_grid_cfg& gcfg, const ttgbf_cross_cfg& xcfg, const ttgbf_run_cfg& rc,
+                  ttgbf_filter_io* io, int32_t* kstep, const double* Z, const int32_t* probes, int nprobes,
+                  const int32_t* seeds, int nseeds, ttgbf_tt* hdr, double* state, int64_t cap, ttgbf_diag* dg,
+                  ttgbf_step_rec* rec, StageSmem S) {
+  const int d = model.d, b = model.b;
+  GeomOut* go;
+  ALLOC(go, GeomOut, 1, ar);
+  const size_t m0 = ar.mark();
+  for (int s = 0; s < rc.steps; ++s) {
+    ttgbf_step_rec* R = rec + s;
+    if (!io->active) {
+      if (c.leader()) {
+        for (int k = 0; k < MAXD; ++k) io->cur[k] = rc.prior_grid[k];
+        *kstep = 0;
+        dg->clipped_mass = 0.0;
+      }
+      c.sync();
+      const int st = stage_prior(c, ar, model, prior, gcfg, xcfg, *io, probes, nprobes, hdr, state, cap, dg, S);
+      ar.release(m0);
+      if (st) {
+        if (c.leader()) { R->status = -1; R->k = -1; }
+        c.sync();
+        continue;
+      }
+      if (c.leader()) io->active = 1;
+      c.sync();
+    }
+    const int kk = *kstep;
+    if (c.leader()) {
+      for (int i = 0; i < b; ++i) io->z[i] = Z[(int64_t)kk * b + i];
+      io->has_z = 1;
+      dg->clipped_mass = 0.0;
+      dg->outlier = 0;
+      R->k = kk;
+      for (int q = 0; q < 3; ++q) dg->cross[q].calls = 0;
+      for (int sl = 0; sl < 8; ++sl)
+        for (int k = 0; k <= TTGBF_MAXD; ++k) dg->ranks[sl][k] = 0;
+    }
+    c.sync();
+    int st = stage_measure(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S);
+    ar.release(m0);
+    if (!st) {
+      int gst = 0;
+      if (c.leader()) {
+        double dv = 1.0;
+        for (int k = 0; k < d; ++k)
+          dv *= (axis_at(io->cur[k], io->cur[k].n - 1) - axis_at(io->cur[k], 0)) / (double)(io->cur[k].n - 1);
+        if (!geom_moments(dg->raw_moments, d, dv, go)) {
+          gst = E_DEGENERATE;
+        } else if (!geom_redesign(go, d, model.F, model.Q, model.Finv, rc.n_per_axis, rc.sigma_mult, io->filt,
+                                  io->pred)) {
+          gst = E_ARG;
+        } else {
+          for (int i = 0; i < d; ++i) { R->mean[i] = go->mean[i]; R->cov_diag[i] = go->cov[i * d + i]; }
+          R->spd_fixed = go->spd_fixed;
+        }
+      }
+      st = (int)bcast_i(c, gst);
+    }
+    if (!st) {
+      st = stage_time(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S);
+      ar.release(m0);
+    }
+    if (c.leader()) {
+      R->status = st;
+      R->outlier = dg->outlier;
+      R->mass_before_norm = dg->mass_before_norm;
+      R->clipped_mass = dg->clipped_mass;
+      for (int q = 0; q < 3; ++q) R->calls[q] = dg->cross[q].calls;
+      for (int sl = 0; sl < 8; ++sl)
+        for (int k = 0; k <= TTGBF_MAXD; ++k) R->ranks[sl][k] = dg->ranks[sl][k];
+      if (st) {
+        io->active = 0;
+      } else {
+        for (int k = 0; k < MAXD; ++k) io->cur[k] = io->pred[k];
+        *kstep = kk + 1;
+        if (kk + 1 >= rc.kf) io->active = 0;
+      }
+    }
+    c.sync();
+  }
   return OK;
 }
 

@@ -147,4 +147,103 @@ HD void pcg_choice(Pcg64& g, int64_t pop, int64_t size, int64_t* out, uint64_t* 
   }
 }
 
+// Cooperative form of pcg_choice with identical output and stream use.
+// All CTA threads call it; warp 0 does the work (lane 0 draws).
+//  * tail shuffle: the virtual arange(pop) lives in `disp` (pop int32 entries,
+//    -1 = untouched; restored to -1 on return).  Draws are made 32 at a
+//    time, the 32 pairs of displacement loads are issued by 32 lanes at once,
+//    then lane 0 resolves the batch in order against its own pending stores.
+//  * Floyd: the probing set lives in shared memory when it fits (sset).
+// jb: >= 128 int64 of shared scratch; touch: >= size int64 (global).
+HDN void choice_coop(const Ctx& c, Pcg64* g, int64_t pop, int64_t size, int64_t* out, int32_t* disp,
+                     uint64_t* sset, int64_t sset_words, uint64_t* gset, int64_t* jb, int64_t* touch) {
+#if ENGINE_DEVICE
+  const int lane = c.tid & 31;
+  const bool w0 = c.tid < 32;
+  const int stride = 32;
+#else
+  const int lane = 0;
+  const bool w0 = true;
+  const int stride = 1;
+#endif
+  if (pop > 10000 && size > pop / 50) {
+    int64_t first = pop - size;
+    if (first < 1) first = 1;
+    const int64_t nsteps = pop - first;
+    if (w0) {
+      int64_t* ld = jb + 32;
+      int64_t* ldi = jb + 64;
+      for (int64_t i0 = pop - 1; i0 >= first; i0 -= 32) {
+        const int cnt = (int)lmin(32, i0 - first + 1);
+        if (lane == 0)
+          for (int t = 0; t < cnt; ++t) jb[t] = (int64_t)pcg_bounded(*g, (uint64_t)(i0 - t));
+#if ENGINE_DEVICE
+        __syncwarp();
+#endif
+        for (int t = lane; t < cnt; t += stride) {
+          ld[t] = disp[jb[t]];
+          ldi[t] = disp[i0 - t];
+        }
+#if ENGINE_DEVICE
+        __syncwarp();
+#endif
+        if (lane == 0) {
+          int64_t sp[32], sv[32];
+          int ns = 0;
+          for (int t = 0; t < cnt; ++t) {
+            const int64_t i = i0 - t, j = jb[t];
+            int64_t vj = ld[t] < 0 ? j : ld[t];
+            int64_t vi = ldi[t] < 0 ? i : ldi[t];
+            for (int q = ns - 1; q >= 0; --q)
+              if (sp[q] == j) { vj = sv[q]; break; }
+            for (int q = ns - 1; q >= 0; --q)
+              if (sp[q] == i) { vi = sv[q]; break; }
+            int q = 0;
+            while (q < ns && sp[q] != j) ++q;
+            sp[q] = j;
+            sv[q] = vi;
+            if (q == ns) ++ns;
+            if (i >= pop - size) out[i - (pop - size)] = vj;
+            touch[(pop - 1) - i] = j;
+          }
+          for (int q = 0; q < ns; ++q) disp[sp[q]] = (int32_t)sv[q];
+        }
+#if ENGINE_DEVICE
+        __syncwarp();
+#endif
+      }
+    }
+    c.sync();
+    for (int64_t q = c.tid; q < nsteps; q += c.nt) disp[touch[q]] = -1;
+    c.sync();
+    return;
+  }
+  if (c.leader()) {
+    const uint64_t mask = gen_mask((uint64_t)(1.2 * (double)size));
+    uint64_t* hs = (int64_t)(mask + 1) <= sset_words ? sset : gset;
+    for (uint64_t i = 0; i <= mask; ++i) hs[i] = ~0ull;
+    for (int64_t j = pop - size; j < pop; ++j) {
+      uint64_t val = pcg_bounded(*g, (uint64_t)j);
+      uint64_t loc = val & mask;
+      while (hs[loc] != ~0ull && hs[loc] != val) loc = (loc + 1) & mask;
+      if (hs[loc] == ~0ull) {
+        hs[loc] = val;
+        out[j - pop + size] = (int64_t)val;
+      } else {
+        loc = (uint64_t)j & mask;
+        while (hs[loc] != ~0ull) loc = (loc + 1) & mask;
+        hs[loc] = (uint64_t)j;
+        out[j - pop + size] = j;
+      }
+    }
+    for (int64_t i = size - 1; i >= 1; --i) {
+      int64_t j = (int64_t)pcg_bounded(*g, (uint64_t)i);
+      int64_t t = out[j];
+      out[j] = out[i];
+      out[i] = t;
+    }
+  }
+  c.sync();
+}
+
 }  // namespace tg

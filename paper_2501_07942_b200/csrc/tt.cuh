@@ -6,6 +6,10 @@
 #pragma once
 #include "common.cuh"
 #include "linalg.cuh"
+#include "la2.cuh"
+#if defined(ENGINE_HOSTSIM) && defined(ENGINE_TRACE)
+#include <stdio.h>
+#endif
 
 namespace tg {
 
@@ -172,11 +176,57 @@ HD void axis_cell(const AxisGeom& g, double x, int* cell, double* frac, bool* in
 
 // generic chain evaluation: `slice(k, a, b)` returns core_k[a, i_k, b] for the
 // point; K points; out[K]
+#if ENGINE_DEVICE
+// Warp-per-point chain with the running row vector held in registers: lane l
+// owns entries l, l+32, ... (S slots); v[a] is broadcast by shuffle and each
+// lane accumulates its output columns from coalesced core-row loads.
+template <int S, class Slice>
+__device__ __forceinline__ void chain_regs(const Ctx& c, const TT& t, int64_t K, Slice& slice, double* out) {
+  const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
+  for (int64_t p = warp; p < K; p += nwarps) {
+    double v[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) v[s] = (s == 0 && lane == 0) ? 1.0 : 0.0;
+    bool dead = false;
+    for (int k = 0; k < t.d; ++k) {
+      const int rl = t.r[k], rr = t.r[k + 1];
+      if (!slice.prepare(k, p)) { dead = true; break; }
+      double acc[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) acc[s] = 0.0;
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        if (s * 32 < rl) {
+          const int amax = imin(32, rl - s * 32);
+          for (int l = 0; l < amax; ++l) {
+            const double va = __shfl_sync(0xffffffffu, v[s], l);
+            const int a = s * 32 + l;
+#pragma unroll
+            for (int q = 0; q < S; ++q) {
+              const int b = q * 32 + lane;
+              if (b < rr) acc[q] = fma(va, slice.at(k, a, b), acc[q]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < S; ++s) v[s] = acc[s];
+    }
+    const double r0 = __shfl_sync(0xffffffffu, v[0], 0);
+    if (lane == 0) out[p] = dead ? 0.0 : r0;
+  }
+  c.sync();
+}
+#endif
+
 template <class Slice>
 HDN void tt_chain_eval(const Ctx& c, const TT& t, int64_t K, Slice slice, double* out, double* sm) {
   int maxr = 1;
   for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
 #if ENGINE_DEVICE
+  if (maxr <= 32) { chain_regs<1>(c, t, K, slice, out); return; }
+  if (maxr <= 64) { chain_regs<2>(c, t, K, slice, out); return; }
+  if (maxr <= 128) { chain_regs<4>(c, t, K, slice, out); return; }
   const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
   double* v = sm + (int64_t)warp * 2 * maxr;
   double* w = v + maxr;
@@ -340,6 +390,7 @@ HD int keep_rank(const double* s, int k, double delta, int cap, double* tail) {
 HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, double** U_out,
                             double** s_out, double** Vt_out, int* kk_out, double* sm) {
   const int kk = imin(m, n);
+  PROF(c, 8);
   double *U, *s, *Vt;
   ALLOC(U, double, (int64_t)m * kk, ar);
   ALLOC(s, double, kk, ar);
@@ -367,13 +418,13 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
   double* Z = Y;
   int zr = yr;
   double* Qy = nullptr;
+  double* Tq = nullptr;
   if (yr > 2 * yc && yc > 1) {
-    double *tau, *T;
+    double* tau;
     ALLOC(tau, double, yc, ar);
-    ALLOC(T, double, QR_NB * QR_NB, ar);
-    CK(qr_householder(c, Y, yr, yr, yc, tau, T, sm));
-    ALLOC(Qy, double, (int64_t)yr * yc, ar);
-    CK(qr_form_q(c, Y, yr, yr, yc, tau, Qy, yr, T, sm));
+    ALLOC(Tq, double, (int64_t)((yc + NB - 1) / NB) * NB * NB, ar);
+    CK(geqrf_nb(c, ar, Y, yr, yr, yc, tau, Tq, sm));
+    Qy = Y;   // reflectors; Q is applied implicitly below
     ALLOC(Z, double, (int64_t)yc * yc, ar);
     for (int64_t e = c.tid; e < (int64_t)yc * yc; e += c.nt) {
       const int i = (int)(e % yc), j = (int)(e / yc);
@@ -389,14 +440,13 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
   double* Uy;
   ALLOC(Uy, double, (int64_t)yr * kk, ar);
   if (Qy) {
-    double* Zp;
-    ALLOC(Zp, double, (int64_t)zr * kk, ar);
-    for (int64_t e = c.tid; e < (int64_t)zr * kk; e += c.nt) {
-      const int i = (int)(e % zr), j = (int)(e / zr);
-      Zp[e] = Z[i + (int64_t)perm[j] * zr];
+    // Uy = Q [Z[:, perm]; 0]
+    for (int64_t e = c.tid; e < (int64_t)yr * kk; e += c.nt) {
+      const int i = (int)(e % yr), j = (int)(e / yr);
+      Uy[e] = (i < zr) ? Z[i + (int64_t)perm[j] * zr] : 0.0;
     }
     c.sync();
-    gemm(c, yr, kk, zr, 1.0, Qy, 1, yr, Zp, 1, zr, 0.0, Uy, 1, yr, sm);
+    CK(apply_q(c, ar, Qy, yr, yr, yc, Tq, false, Uy, yr, kk, sm));
   } else {
     for (int64_t e = c.tid; e < (int64_t)yr * kk; e += c.nt) {
       const int i = (int)(e % yr), j = (int)(e / yr);
@@ -437,37 +487,49 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
 // ---------------------------------------------------------------------------
 HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT& out, double* sm) {
   const int d = in.d;
+  PROF(c, 7);
   if (d == 1) return tt_clone(c, ar, in, out);
   size_t mk0 = ar.mark();
+  // Right-to-left: blocked Householder QR of core_k^T (rows (i, gamma), cols
+  // alpha).  The reflectors stay in place (Q is never formed); R^T is carried
+  // into core k-1.
   TT w;
   CK(tt_clone(c, ar, in, w));
-  double* T;
-  ALLOC(T, double, QR_NB * QR_NB, ar);
+  double* taus[MAXD];
+  double* Ts[MAXD];
+  int mrow[MAXD], kq[MAXD];
   for (int k = d - 1; k >= 1; --k) {
     const int rl = w.r[k], n = w.n[k], rr = w.r[k + 1];
     const int m = n * rr;
     const int kk = imin(m, rl);
+    ALLOC(taus[k], double, kk, ar);
+    ALLOC(Ts[k], double, (int64_t)((kk + NB - 1) / NB) * NB * NB, ar);
+    {
+      PROF(c, 9);
+      CK(geqrf_nb(c, ar, w.c[k], m, m, rl, taus[k], Ts[k], sm));
+    }
+    mrow[k] = m;
+    kq[k] = kk;
+#if defined(ENGINE_HOSTSIM) && defined(ENGINE_TRACE)
+    fprintf(stderr, "RL k=%d m=%d rl=%d kk=%d A:", k, m, rl, kk);
+    for (int q = 0; q < m * rl; ++q) fprintf(stderr, " %.4f", w.c[k][q]);
+    fprintf(stderr, " T: %.4f %.4f %.4f", Ts[k][0], Ts[k][NB], Ts[k][NB + 1]);
+    fprintf(stderr, " tau:");
+    for (int q = 0; q < kk; ++q) fprintf(stderr, " %.4f", taus[k][q]);
+    fprintf(stderr, "\n");
+#endif
     size_t mk = ar.mark();
-    double *tau, *Q, *Rm;
-    ALLOC(tau, double, kk, ar);
-    CK(qr_householder(c, w.c[k], m, m, rl, tau, T, sm));
+    double *Rm, *nc;
     ALLOC(Rm, double, (int64_t)kk * rl, ar);   // R (kk x rl) row-major
     for (int64_t e = c.tid; e < (int64_t)kk * rl; e += c.nt) {
       const int i = (int)(e / rl), j = (int)(e % rl);
       Rm[e] = (i <= j) ? w.c[k][i + (int64_t)j * m] : 0.0;
     }
-    ALLOC(Q, double, (int64_t)m * kk, ar);
-    c.sync();
-    CK(qr_form_q(c, w.c[k], m, m, kk, tau, Q, m, T, sm));
-    // new core k = Q^T reshaped (kk, n, rr): Q col-major (m x kk) == C-order
-    par_copy(c, w.c[k], Q, (int64_t)m * kk);
-    // core k-1 <- core k-1 x_3 R^T : (rpp*n', rl) @ R^T (rl x kk)
     const int rpp = w.r[k - 1], np_ = w.n[k - 1];
-    double* nc;
     ALLOC(nc, double, (int64_t)rpp * np_ * kk, ar);
     c.sync();
-    gemm(c, rpp * np_, kk, rl, 1.0, w.c[k - 1], rl, 1, Rm, 1, rl, 0.0, nc, kk, 1, sm);
-    // cores may only shrink: copy back into the existing buffers
+    // core k-1 <- core k-1 x_3 R^T : (rpp*n', rl) @ R^T (rl x kk)
+    gemm_t<64>(c, rpp * np_, kk, rl, 1.0, Mat{w.c[k - 1], rl, 1}, Mat{Rm, 1, rl}, 0.0, nc, kk, 1, sm);
     par_copy(c, w.c[k - 1], nc, (int64_t)rpp * np_ * kk);
     c.sync();
     w.r[k] = kk;
@@ -488,56 +550,118 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
     return OK;
   }
   const double delta = tol * nrm / sqrt((double)(d - 1));
-  for (int k = 0; k < d - 1; ++k) {
-    const int rl = w.r[k], n = w.n[k], rr = w.r[k + 1];
-    const int m = rl * n;
+  // Left-to-right: X_k = carry Q_k^T, computed as (Q_k [carry^T; 0])^T, then
+  // truncated SVD.  New cores are appended in the arena (compacted at the end).
+  TT res;
+  res.d = d;
+  for (int k = 0; k < d; ++k) res.n[k] = w.n[k];
+  res.r[0] = 1;
+  res.r[d] = 1;
+  double* carry = nullptr;
+  int rprev = 1;
+  for (int k = 0; k < d; ++k) {
+    const int n = w.n[k], rr = w.r[k + 1];
+    const int mx = rprev * n;          // rows of X_k
     size_t mk = ar.mark();
+    double* X;                         // row-major (rprev*n) x rr
+    if (k == 0) {
+      X = w.c[0];
+    } else {
+      const int m = mrow[k], kk = kq[k];
+      double* Y;                       // col-major m x rprev
+      ALLOC(Y, double, (int64_t)m * rprev, ar);
+      for (int64_t e = c.tid; e < (int64_t)m * rprev; e += c.nt) {
+        const int64_t r = e % m;
+        const int a = (int)(e / m);
+        Y[e] = (r < kk) ? carry[(int64_t)a * kk + r] : 0.0;
+      }
+      c.sync();
+#if defined(ENGINE_HOSTSIM) && defined(ENGINE_TRACE)
+      fprintf(stderr, "Yin:");
+      for (int q = 0; q < m * rprev; ++q) fprintf(stderr, " %.4f", Y[q]);
+      fprintf(stderr, "\n");
+#endif
+      CK(apply_q(c, ar, w.c[k], m, m, kk, Ts[k], false, Y, m, rprev, sm));
+#if defined(ENGINE_HOSTSIM) && defined(ENGINE_TRACE)
+      fprintf(stderr, "LR k=%d A:", k);
+      for (int q = 0; q < m * kk; ++q) fprintf(stderr, " %.4f", w.c[k][q]);
+      fprintf(stderr, " T: %.4f %.4f %.4f | ", Ts[k][0], Ts[k][NB], Ts[k][NB + 1]);
+      fprintf(stderr, "k=%d m=%d kk=%d rprev=%d carry:", k, m, kk, rprev);
+      for (int q = 0; q < rprev * kk; ++q) fprintf(stderr, " %.4f", carry[q]);
+      fprintf(stderr, "\n Y:");
+      for (int q = 0; q < m * rprev; ++q) fprintf(stderr, " %.4f", Y[q]);
+      fprintf(stderr, "\n");
+#endif
+      ALLOC(X, double, (int64_t)mx * rr, ar);
+      for (int64_t e = c.tid; e < (int64_t)mx * rr; e += c.nt) {
+        const int64_t row = e / rr;
+        const int g = (int)(e % rr);
+        const int a = (int)(row / n), i = (int)(row % n);
+        X[e] = Y[((int64_t)i * rr + g) + (int64_t)a * m];
+      }
+      c.sync();
+    }
+    if (k == d - 1) {
+      double* core;
+      ALLOC(core, double, (int64_t)mx, ar);
+      par_copy(c, core, X, mx);
+      c.sync();
+      res.c[k] = core;
+      break;
+    }
     double *U, *s, *Vt;
     int kk;
-    CK(svd_rowmajor(c, ar, w.c[k], m, rr, &U, &s, &Vt, &kk, sm));
+    CK(svd_rowmajor(c, ar, X, mx, rr, &U, &s, &Vt, &kk, sm));
     double* tail;
     ALLOC(tail, double, kk, ar);
     int rnew = 0;
     if (c.leader()) rnew = keep_rank(s, kk, delta, cap, tail);
     rnew = (int)bcast_i(c, rnew);
-    // core k = U[:, :rnew] (C-order (rl, n, rnew))
-    for (int64_t e = c.tid; e < (int64_t)m * rnew; e += c.nt) {
+    // stash U[:, :rnew] and carry = s V^T[:rnew] above the temporaries, then
+    // move them down to `mk`
+    double *core, *cr;
+    ALLOC(core, double, (int64_t)mx * rnew, ar);
+    ALLOC(cr, double, (int64_t)rnew * rr, ar);
+    for (int64_t e = c.tid; e < (int64_t)mx * rnew; e += c.nt) {
       const int64_t i = e / rnew;
       const int j = (int)(e % rnew);
-      w.c[k][e] = U[i + (int64_t)j * m];
+      core[e] = U[i + (int64_t)j * mx];
     }
-    // carry = s[:rnew, None] * Vt[:rnew]  (rnew x rr); core k+1 <- carry @ core
-    double* carry;
-    ALLOC(carry, double, (int64_t)rnew * rr, ar);
-    for (int64_t e = c.tid; e < (int64_t)rnew * rr; e += c.nt) carry[e] = s[e / rr] * Vt[e];
-    const int n2 = w.n[k + 1], r2 = w.r[k + 2];
-    double* nc;
-    ALLOC(nc, double, (int64_t)rnew * n2 * r2, ar);
+    for (int64_t e = c.tid; e < (int64_t)rnew * rr; e += c.nt) cr[e] = s[e / rr] * Vt[e];
     c.sync();
-    gemm(c, rnew, n2 * r2, rr, 1.0, carry, rr, 1, w.c[k + 1], (int64_t)n2 * r2, 1, 0.0, nc,
-         (int64_t)n2 * r2, 1, sm);
-    par_copy(c, w.c[k + 1], nc, (int64_t)rnew * n2 * r2);
-    c.sync();
-    w.r[k + 1] = rnew;
     ar.release(mk);
+    double *core2, *cr2;
+    ALLOC(core2, double, (int64_t)mx * rnew, ar);
+    ALLOC(cr2, double, (int64_t)rnew * rr, ar);
+    // destinations are below the sources: chunked forward copies
+    for (int pass = 0; pass < 2; ++pass) {
+      double* dst = pass ? cr2 : core2;
+      const double* src = pass ? cr : core;
+      const int64_t sz = pass ? (int64_t)rnew * rr : (int64_t)mx * rnew;
+      if (dst == src) continue;
+      const int64_t chunk = (int64_t)(src - dst);
+      for (int64_t s0 = 0; s0 < sz; s0 += chunk) {
+        const int64_t s1 = lmin(sz, s0 + chunk);
+        for (int64_t e = s0 + c.tid; e < s1; e += c.nt) dst[e] = src[e];
+        c.sync();
+      }
+    }
+    c.sync();
+    res.c[k] = core2;
+    res.r[k + 1] = rnew;
+    carry = cr2;
+    rprev = rnew;
   }
-  // move the result to the front of the released region
-  TT res;
-  res.d = d;
-  for (int k = 0; k < d; ++k) res.n[k] = w.n[k];
-  for (int k = 0; k <= d; ++k) res.r[k] = w.r[k];
-  // w's buffers sit right after mk0; compact in order (sizes only shrank)
+  // compact the output cores down to mk0 (each destination precedes its source)
   ar.release(mk0);
   CK(tt_alloc(ar, out, d, res.n, res.r));
   for (int k = 0; k < d; ++k) {
-    // out.c[k] <= w.c[k] in address (same allocation order, smaller sizes):
-    // forward copy is safe in a serial pass, so do it in chunks with syncs.
     const int64_t sz = out.size(k);
-    if (out.c[k] == w.c[k]) continue;
-    const int64_t chunk = (int64_t)(w.c[k] - out.c[k]);
+    if (out.c[k] == res.c[k]) continue;
+    const int64_t chunk = (int64_t)(res.c[k] - out.c[k]);
     for (int64_t s0 = 0; s0 < sz; s0 += chunk) {
       const int64_t s1 = lmin(sz, s0 + chunk);
-      for (int64_t e = s0 + c.tid; e < s1; e += c.nt) out.c[k][e] = w.c[k][e];
+      for (int64_t e = s0 + c.tid; e < s1; e += c.nt) out.c[k][e] = res.c[k][e];
       c.sync();
     }
   }
@@ -553,6 +677,7 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
 HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double tol, int cap,
                            TT& out, double* sm) {
   const int d = K.d;
+  PROF(c, 14);
   size_t mk0 = ar.mark();
   TT P;
   {
@@ -671,6 +796,7 @@ HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double to
 // ---------------------------------------------------------------------------
 HDN int tt_negative_mass(const Ctx& c, Arena& ar, const TT& t, int64_t guard, const int32_t* probes,
                                 int nprobes, double* result, double* sm) {
+  PROF(c, 15);
   int64_t total = 1;
   bool big = false;
   for (int k = 0; k < t.d; ++k) {

@@ -100,3 +100,24 @@ def measure_fp64_peak(torch, device, n=8192, reps=5):
         best = min(best, s.elapsed_time(e) / 1e3)
     del a, b
     return 2.0 * n ** 3 / best / 1e12
+
+
+class _Row:
+    """Adapter: a STEP_REC viewed as the (measure, time) diag rows."""
+
+    def __init__(self, rec):
+        self.rec = rec
+
+    def __getitem__(self, key):
+        if key == "ranks":
+            return self.rec["ranks"]
+        if key == "cross":
+            calls = self.rec["calls"]
+            return [{"calls": int(calls[q])} for q in range(3)]
+        return self.rec[key]
+
+
+def rec_flops(rec, d, b, n):
+    """(measure, time) algorithmic FLOPs of one persistent-run step record."""
+    r = _Row(rec)
+    return step_flops(r, r, d, b, n)

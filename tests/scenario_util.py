@@ -104,3 +104,25 @@ def check_primitives(golden, case):
     assert rel(G.tt_eval_at_points(a, og, pts), T.at_points(load_tt(z, f"{case}/a"), og.axes, pts)) <= 1e-13
 
 
+
+
+def compare_scenario_run(golden, name, backend):
+    """The persistent multi-step kernel (device geometry) on a golden scenario."""
+    z = golden("trajectories")
+    sc = SCENARIOS[name]
+    bank = FilterBank(sc["spec"], bank_config(sc), 1, backend=backend)
+    done = int(z[f"{name}/done"])
+    zs = z[f"{name}/z"][None, :, :]
+    recs = bank.run(zs, done, sc["x0_mean"], sc["x0_cov"])[0]
+    rows = []
+    for k in range(done):
+        r = recs[k]
+        assert int(r["status"]) == 0 and int(r["k"]) == k, (k, r["status"], r["k"])
+        d = sc["spec"]["F"].shape[0]
+        rows.append({"step": k, "mean": rel(r["mean"][:d], z[f"{name}/{k}/filt_mean"]),
+                     "cov": rel(r["cov_diag"][:d], np.diag(z[f"{name}/{k}/filt_cov"]))})
+    got = bank.cores(0)
+    ref = load_tt(z, f"{name}/{done - 1}/pred")
+    rows.append({"step": "final", "dens": rel(T.to_full(got), T.to_full(ref)),
+                 "ranks": (T.ranks_of(got), T.ranks_of(ref))})
+    return rows
