@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--batch", type=int, default=148)
+    p.add_argument("--batch", type=int, default=296)   # 2 filter CTAs per SM
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C5")
     p.add_argument("--ws-mb", type=int, default=512)
@@ -245,6 +245,10 @@ def run_ours(args):
     stats["cycles"] = dg["cycles"].sum(axis=0).astype(float)
     stats["prof"] = dg["prof"].sum(axis=0).astype(float)
     stats["ws_peak"] = int(dg["ws_peak"].max())
+    att = recs["status"] >= 0
+    stats["calls"] = {nm: float(recs["calls"][:, :, q][att].mean()) if att.any() else 0.0
+                      for q, nm in enumerate(["likelihood", "kernel", "realign"])}
+    stats["stage_s_per_step"] = (dg["cycles"].sum(axis=0) / 1.965e9 / max(1, int(att.sum()))).round(4).tolist()
     if ok.any():
         i0, s0 = [int(v[0]) for v in np.nonzero(ok)]
         stats["ranks"] = {nm: [int(v) for v in recs[i0, s0]["ranks"][sl][: d + 1]]
@@ -310,6 +314,8 @@ def run_ours(args):
         "engine_prof_share": dict(zip(PROF_NAMES, (stats["prof"] / max(stats["cycles"].sum(), 1)).round(4).tolist())),
         "completed_frac": stats["completed"] / max(1, B * args.steps),
         "ws_peak_mb": stats["ws_peak"] / 2 ** 20,
+        "mean_cross_calls": stats["calls"],
+        "stage_sm_seconds_per_attempted_step": stats["stage_s_per_step"],
         "example_ranks": stats["ranks"],
         "rmse": rmse,
         "clocks": clk.summary(),

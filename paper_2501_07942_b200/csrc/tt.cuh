@@ -480,6 +480,218 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
 }
 
 // ---------------------------------------------------------------------------
+// Rank-revealing truncated SVD of a row-major (m x n) matrix X (read-only).
+// Householder QR with column pivoting (largest remaining column first) is
+// stopped once the Frobenius norm of the unreduced block falls to eps_abs;
+// the p x n leading block [R11 R12] P^T is then factored exactly (QR of its
+// transpose + one-sided Jacobi on the p x p triangle).  Dropping the
+// unreduced block perturbs every singular value by <= eps_abs and the tail
+// energies by <= eps_abs^2, so with eps_abs = 1e-3 * delta the truncation
+// rule of tt_round and the kept subspace are unchanged up to ~1e-3 delta.
+// eps_abs = 0 gives the full SVD.  Outputs as svd_rowmajor with kk = p.
+// ---------------------------------------------------------------------------
+HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double eps_abs, double** U_out,
+                 double** s_out, double** Vt_out, int* kk_out, double* sm) {
+  PROF(c, 8);
+  const int kmax = imin(m, n);
+  // outputs sized for the worst case (p <= kmax), allocated first
+  double *U, *s, *Vt;
+  ALLOC(U, double, (int64_t)m * kmax, ar);
+  ALLOC(s, double, kmax, ar);
+  ALLOC(Vt, double, (int64_t)kmax * n, ar);
+  const size_t mk = ar.mark();
+  double *A, *cn, *tau;
+  int* perm;
+  ALLOC(A, double, (int64_t)m * n, ar);     // col-major copy
+  ALLOC(cn, double, n, ar);
+  ALLOC(tau, double, kmax, ar);
+  ALLOC(perm, int, n, ar);
+  for (int64_t e = c.tid; e < (int64_t)m * n; e += c.nt) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    A[i + (int64_t)j * m] = X[e];
+  }
+  for (int j = c.tid; j < n; j += c.nt) perm[j] = j;
+  c.sync();
+#if ENGINE_DEVICE
+  const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
+#endif
+  // column norms^2 (one warp per column)
+#if ENGINE_DEVICE
+  for (int j = warp; j < n; j += nwarps) {
+    double a = 0.0;
+    for (int r = lane; r < m; r += 32) a = fma(A[r + (int64_t)j * m], A[r + (int64_t)j * m], a);
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) cn[j] = a;
+  }
+#else
+  for (int j = 0; j < n; ++j) {
+    double a = 0.0;
+    for (int r = 0; r < m; ++r) a = fma(A[r + (int64_t)j * m], A[r + (int64_t)j * m], a);
+    cn[j] = a;
+  }
+#endif
+  c.sync();
+  const double eps2 = eps_abs * eps_abs;
+  int p = 0;
+  for (int j = 0; j < kmax; ++j) {
+    // remaining energy and pivot
+    double part = 0.0;
+    ValIdx best{-1.0, 0};
+    for (int q = j + c.tid; q < n; q += c.nt) {
+      part += cn[q];
+      best = vi_better(best, ValIdx{cn[q], q});
+    }
+    const double rem = block_sum(c, part);
+    best = block_argmax(c, best);
+    if (rem <= eps2 || best.v <= 0.0) break;
+    const int pv = (int)best.i;
+    if (pv != j) {
+      for (int r = c.tid; r < m; r += c.nt) {
+        const double t = A[r + (int64_t)j * m];
+        A[r + (int64_t)j * m] = A[r + (int64_t)pv * m];
+        A[r + (int64_t)pv * m] = t;
+      }
+      c.sync();
+      if (c.leader()) {
+        const int t = perm[j]; perm[j] = perm[pv]; perm[pv] = t;
+        const double tc = cn[j]; cn[j] = cn[pv]; cn[pv] = tc;
+      }
+    }
+    c.sync();
+    // reflector of column j (rows j..m-1)
+    double* col = A + (int64_t)j * m;
+    double part2 = 0.0;
+    for (int r = j + 1 + c.tid; r < m; r += c.nt) part2 = fma(col[r], col[r], part2);
+    const double xn = sqrt(block_sum(c, part2));
+    const double alpha = col[j];
+    double t, beta, scal;
+    larfg(alpha, xn, &t, &beta, &scal);
+    for (int r = j + 1 + c.tid; r < m; r += c.nt) col[r] *= scal;
+    c.sync();
+    if (c.leader()) { col[j] = beta; tau[j] = t; }
+    c.sync();
+    // apply to the trailing columns and refresh their norms (rows > j)
+#if ENGINE_DEVICE
+    for (int q = j + 1 + warp; q < n; q += nwarps) {
+      double* cq = A + (int64_t)q * m;
+      double w = 0.0;
+      for (int r = j + lane; r < m; r += 32) w = fma(r == j ? 1.0 : col[r], cq[r], w);
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      w *= t;
+      double nr = 0.0;
+      for (int r = j + lane; r < m; r += 32) {
+        const double v = cq[r] - w * (r == j ? 1.0 : col[r]);
+        cq[r] = v;
+        if (r > j) nr = fma(v, v, nr);
+      }
+      for (int o = 16; o > 0; o >>= 1) nr += __shfl_xor_sync(0xffffffffu, nr, o);
+      if (lane == 0) cn[q] = nr;
+    }
+#else
+    for (int q = j + 1; q < n; ++q) {
+      double* cq = A + (int64_t)q * m;
+      double w = 0.0;
+      for (int r = j; r < m; ++r) w = fma(r == j ? 1.0 : col[r], cq[r], w);
+      w *= t;
+      double nr = 0.0;
+      for (int r = j; r < m; ++r) {
+        const double v = cq[r] - w * (r == j ? 1.0 : col[r]);
+        cq[r] = v;
+        if (r > j) nr = fma(v, v, nr);
+      }
+      cn[q] = nr;
+    }
+#endif
+    c.sync();
+    p = j + 1;
+  }
+  if (p == 0) {   // zero matrix: one zero singular triplet
+    for (int64_t e = c.tid; e < m; e += c.nt) U[e] = (e == 0) ? 1.0 : 0.0;
+    for (int64_t e = c.tid; e < n; e += c.nt) Vt[e] = (e == 0) ? 1.0 : 0.0;
+    if (c.leader()) s[0] = 0.0;
+    c.sync();
+    ar.release(mk);
+    *U_out = U; *s_out = s; *Vt_out = Vt; *kk_out = 1;
+    return OK;
+  }
+  // Bt = (R P^T)^T: n x p col-major, Bt[perm[q], i] = R[i, q] (i <= q)
+  double *Bt, *tq, *Tq, *Z, *Vj, *tmp;
+  int* jp;
+  ALLOC(Bt, double, (int64_t)n * p, ar);
+  for (int64_t e = c.tid; e < (int64_t)n * p; e += c.nt) {
+    const int q = (int)(e % n), i = (int)(e / n);
+    Bt[perm[q] + (int64_t)i * n] = (i <= q) ? A[i + (int64_t)q * m] : 0.0;
+  }
+  c.sync();
+  // QR of Bt (n x p, n >= p): Bt = Q2 R2;  R2^T = B's left factor
+  ALLOC(tq, double, p, ar);
+  ALLOC(Tq, double, (int64_t)((p + NB - 1) / NB) * NB * NB, ar);
+  CK(geqrf_nb(c, ar, Bt, n, n, p, tq, Tq, sm));
+  // Z = R2^T (p x p, col-major) -> one-sided Jacobi on its columns:
+  // R2^T Vj = Uz S  =>  B = R2^T Q2^T = Uz S (Q2 Vj)^T
+  ALLOC(Z, double, (int64_t)p * p, ar);
+  for (int64_t e = c.tid; e < (int64_t)p * p; e += c.nt) {
+    const int i = (int)(e % p), j = (int)(e / p);     // Z(i, j) = R2(j, i)
+    Z[e] = (j <= i) ? Bt[j + (int64_t)i * n] : 0.0;
+  }
+  ALLOC(Vj, double, (int64_t)p * p, ar);
+  ALLOC(tmp, double, p, ar);
+  ALLOC(jp, int, p, ar);
+  c.sync();
+  CK(svd_jacobi(c, Z, p, p, p, Vj, s, jp, tmp));
+  // U = Q1 [Uz[:, perm]; 0]   (m x p);  Q1 = H_0 .. H_{p-1} of the pivoted QR
+  for (int64_t e = c.tid; e < (int64_t)m * p; e += c.nt) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    U[e] = (i < p) ? Z[i + (int64_t)jp[j] * p] : 0.0;
+  }
+  c.sync();
+  for (int jj = p - 1; jj >= 0; --jj) {   // apply H_jj (rows jj..m-1) to all p columns
+    const double* v = A + (int64_t)jj * m;
+    const double t2 = tau[jj];
+    if (t2 == 0.0) continue;
+#if ENGINE_DEVICE
+    for (int q = warp; q < p; q += nwarps) {
+      double* uq = U + (int64_t)q * m;
+      double w = 0.0;
+      for (int r = jj + lane; r < m; r += 32) w = fma(r == jj ? 1.0 : v[r], uq[r], w);
+      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+      w *= t2;
+      for (int r = jj + lane; r < m; r += 32) uq[r] -= w * (r == jj ? 1.0 : v[r]);
+    }
+#else
+    for (int q = 0; q < p; ++q) {
+      double* uq = U + (int64_t)q * m;
+      double w = 0.0;
+      for (int r = jj; r < m; ++r) w = fma(r == jj ? 1.0 : v[r], uq[r], w);
+      w *= t2;
+      for (int r = jj; r < m; ++r) uq[r] -= w * (r == jj ? 1.0 : v[r]);
+    }
+#endif
+    c.sync();
+  }
+  // Vt[i, :] = (Q2 [Vj[:, jp[i]]; 0])^T
+  double* Vm;
+  ALLOC(Vm, double, (int64_t)n * p, ar);
+  for (int64_t e = c.tid; e < (int64_t)n * p; e += c.nt) {
+    const int i = (int)(e % n), j = (int)(e / n);
+    Vm[e] = (i < p) ? Vj[i + (int64_t)jp[j] * p] : 0.0;
+  }
+  c.sync();
+  CK(apply_q(c, ar, Bt, n, n, p, Tq, false, Vm, n, p, sm));
+  for (int64_t e = c.tid; e < (int64_t)p * n; e += c.nt) {
+    const int i = (int)(e / n), q = (int)(e % n);
+    Vt[e] = Vm[q + (int64_t)i * n];
+  }
+  c.sync();
+  ar.release(mk);
+  *U_out = U;
+  *s_out = s;
+  *Vt_out = Vt;
+  *kk_out = p;
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
 // TT rounding (tensor_train.py:327-360): right-to-left Householder QR, then
 // left-to-right truncated SVD with the reference's rule and sweep direction.
 // The result is written into `out` (allocated here, after the temporaries are
@@ -611,7 +823,7 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
     }
     double *U, *s, *Vt;
     int kk;
-    CK(svd_rowmajor(c, ar, X, mx, rr, &U, &s, &Vt, &kk, sm));
+    CK(svd_rrqr(c, ar, X, mx, rr, 1e-3 * delta, &U, &s, &Vt, &kk, sm));
     double* tail;
     ALLOC(tail, double, kk, ar);
     int rnew = 0;
