@@ -45,7 +45,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--batch", type=int, default=296)   # 2 filter CTAs per SM
+    p.add_argument("--batch", type=int, default=1184)  # filters per GPU (4 per resident CTA slot)
+    p.add_argument("--slots", type=int, default=296)   # resident CTAs: 2 per SM x 148
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C5")
     p.add_argument("--ws-mb", type=int, default=512)
@@ -208,7 +209,7 @@ def run_ours(args):
     bcfg = BankConfig(n_per_axis=g["n_per_axis"], sigma_mult=g["sigma_mult"], round_tol=g["round_tol"],
                       round_max_rank=g["round_max_rank"], tol=x["tol"], max_rank=x["max_rank"],
                       rng_seed=x["rng_seed"], ws_bytes=args.ws_mb << 20, state_doubles=1 << 19,
-                      cache_cap=1 << 20)
+                      cache_cap=1 << 20, ws_slots=args.slots)
     d = cfg["spec"]["F"].shape[0]
     b = np.atleast_2d(cfg["spec"]["R"]).shape[0]
     n = g["n_per_axis"]
@@ -300,6 +301,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded trajectories, SeedSequence((2024, run, 0)))",
         "config": {"workload": WORKLOAD, "filters_per_gpu": B, "runs": world * B, "parallelism": f"dp{world}",
+                   "workspace_slots": args.slots,
                    "l2": "per-filter working sets stream from HBM (batch footprint >> 126 MB L2)",
                    "completed_steps": done_all, "restarts": stats["restarts"], "failed_steps": stats["failed"]},
         "gpu_launches": len(bank.timeline),

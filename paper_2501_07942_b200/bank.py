@@ -51,6 +51,7 @@ class BankConfig:
     ws_bytes: int = 256 << 20
     state_doubles: int = 1 << 20
     cache_cap: int = 1 << 20
+    ws_slots: int = 0          # persistent run: workspace slots (0 = one per filter)
 
     def grid_cfg(self):
         return _abi.GridCfg(self.round_tol, int(self.round_max_rank or 0),
@@ -157,7 +158,9 @@ class FilterBank:
         self.io_dev = backend.empty(self.io.nbytes)
         self.hdr = backend.empty(n * _abi.TT.itemsize)
         self.state = backend.empty(n * cfg.state_doubles * 8)
-        self.ws = backend.empty(n * cfg.ws_bytes)
+        self.nslots = min(n, cfg.ws_slots) if cfg.ws_slots > 0 else n
+        self.ws = backend.empty(self.nslots * cfg.ws_bytes)
+        self.slot_busy = backend.upload(np.zeros(max(1, self.nslots), dtype=np.int32))
         self.diag_dev = backend.empty(n * _abi.DIAG.itemsize)
         self.grids: list[geo.Axes | None] = [None] * n
         self.alive = np.zeros(n, dtype=bool)
@@ -166,6 +169,11 @@ class FilterBank:
         self.bytes_d2h = 0
 
     # -- helpers ----------------------------------------------------------------
+    def _need_slot_per_filter(self):
+        if self.nslots < self.count:
+            raise RuntimeError("stage-wise calls need one workspace slot per filter; use run() "
+                               "or BankConfig(ws_slots=0)")
+
     def _push_io(self):
         self.be.upload_into(self.io_dev, self.io)
         self.bytes_h2d += self.io.nbytes
@@ -194,6 +202,7 @@ class FilterBank:
     # -- stages -----------------------------------------------------------------
     def init_prior(self, mean, cov, which=None):
         """initial_pmd_tt for every filter in ``which`` (default all)."""
+        self._need_slot_per_filter()
         which = np.arange(self.count) if which is None else np.asarray(which)
         grid = geo.design_grid(mean, cov, self.cfg.n_per_axis, self.cfg.sigma_mult)
         prior = self.be.upload(gauss_record(mean, cov))
@@ -215,6 +224,7 @@ class FilterBank:
 
     def measure(self, z, has_z=None):
         """measurement_update + raw moments for all alive filters."""
+        self._need_slot_per_filter()
         z = np.atleast_2d(np.asarray(z, dtype=float))
         self.io["active"] = self.alive.astype(np.int32)
         self.io["z"][:, :self.b] = z
@@ -248,6 +258,7 @@ class FilterBank:
         return out
 
     def time_update(self, geom):
+        self._need_slot_per_filter()
         act = np.zeros(self.count, dtype=np.int32)
         for i, (st, _) in geom.items():
             if st == "ok":
@@ -326,7 +337,7 @@ class FilterBank:
         self._launch("ttgbf_filter_run", self.lib.ttgbf_filter_run, self.model.ptr, prior_dev.ptr, self.gcfg,
                      self.xcfg, rc, self.io_dev.ptr, self.kstep_dev.ptr, zb.ptr, self.count, pr, npr, sd, nsd,
                      self.hdr.ptr, self.state.ptr, self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes,
-                     self.diag_dev.ptr, rec.ptr, self.be.stream_ptr)
+                     self.slot_busy.ptr, self.nslots, self.diag_dev.ptr, rec.ptr, self.be.stream_ptr)
         recs = self.be.download(rec, _abi.STEP_REC, self.count * steps).reshape(self.count, steps)
         self.io = self.be.download(self.io_dev, _abi.FILTER_IO, self.count)
         self.bytes_d2h += recs.nbytes + self.io.nbytes

@@ -137,11 +137,23 @@ int ttgbf_filter_time_update(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgb
 int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
                      ttgbf_run_cfg rcfg, ttgbf_filter_io* io, int32_t* kstep, const double* Z, int nfilt,
                      const int32_t* probes, int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr,
-                     double* state, int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag,
-                     ttgbf_step_rec* rec, void* stream) {
-  if (rcfg.steps < 0 || rcfg.kf < 1) return TTGBF_E_ARG;
+                     double* state, int64_t state_cap, void* ws, int64_t ws_bytes, int32_t* slot_busy,
+                     int nslots, ttgbf_diag* diag, ttgbf_step_rec* rec, void* stream) {
+  if (rcfg.steps < 0 || rcfg.kf < 1 || nslots < 1) return TTGBF_E_ARG;
   auto f = LAMBDA(const Ctx& c0, int i, double* smem) {
-    Arena ar = make_arena(ws, ws_bytes, i);
+    // claim a free workspace slot for this CTA's lifetime
+    int slot = 0;
+    if (c0.leader()) {
+      slot = i % nslots;
+#if ENGINE_DEVICE
+      while (atomicCAS(&slot_busy[slot], 0, 1) != 0) slot = (slot + 1) % nslots;
+#else
+      while (slot_busy[slot] != 0) slot = (slot + 1) % nslots;
+      slot_busy[slot] = 1;
+#endif
+    }
+    slot = (int)bcast_i(c0, slot);
+    Arena ar = make_arena(ws, ws_bytes, slot);
     ttgbf_diag* dg = diag + i;
     Ctx c = c0;
     c.prof = dg->prof;
@@ -155,6 +167,13 @@ int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_g
                        probes, nprobes, seeds, nseeds, state_hdr + i, state + (int64_t)i * state_cap, state_cap, dg,
                        rec + (int64_t)i * rcfg.steps, make_stage_smem(smem));
     if (c.leader()) { dg->status = st; dg->ws_peak = (int64_t)ar.peak; }
+    c.sync();
+#if ENGINE_DEVICE
+    __threadfence();
+    if (c.leader()) atomicExch(&slot_busy[slot], 0);
+#else
+    slot_busy[slot] = 0;
+#endif
   };
   return launch(nfilt, f, stream);
 }

@@ -94,11 +94,6 @@ HDN int body_eval_many(const Ctx& c, const ttgbf_tt* h, const double* data, cons
   return OK;
 }
 
-struct PtsFn {
-  const double* pts;
-  int d;
-  HD double operator()(int64_t p, int k) const { return pts[p * d + k]; }
-};
 
 HDN int body_eval_points(const Ctx& c, Arena& ar, const ttgbf_tt* h, const double* data,
                                 const ttgbf_axis* axes, const double* pts, int64_t K, double* out, double* sm) {

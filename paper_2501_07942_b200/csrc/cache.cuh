@@ -229,12 +229,12 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
     double* nv = C->vals + base;
     PROF(c, 1);
     if (spec.kind == EV_REALIGN) {
-      struct RPt {
-        const EvalSpec* s;
-        const int32_t* ix;
-        HD double operator()(int64_t p, int k) const { return realign_coord(*s, ix + p * s->d, k); }
-      };
-      PointSlice<RPt> ps{&spec.conv, spec.geo, RPt{&spec, uidx}, 0, 0.0};
+      // pull the predictive nodes back once: coords = F^{-1} y (filters.py:973)
+      double* coords;
+      ALLOC(coords, double, M * d, ar);
+      for (int64_t e = c.tid; e < M * d; e += c.nt) coords[e] = realign_coord(spec, uidx + (e / d) * d, (int)(e % d));
+      c.sync();
+      PointSlice<PtsFn> ps{&spec.conv, spec.geo, PtsFn{coords, d}, 0, 0.0};
       tt_chain_eval(c, spec.conv, M, ps, nv, sm);
     } else {
       for (int64_t j = c.tid; j < M; j += c.nt) nv[j] = eval_point(spec, uidx + j * d);

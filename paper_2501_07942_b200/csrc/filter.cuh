@@ -132,7 +132,8 @@ HD void put_cross(ttgbf_cross_info* o, const CrossInfo& i) {
   o->converged = i.converged;
 }
 
-// _finalize_tt (filters.py:454-479): round -> mass -> scale -> negative mass
+// _finalize_tt (filters.py:454-479): round -> mass -> scale -> negative mass.
+// The input TT is a temporary and is consumed (rounded in place).
 HDN int finalize_tt(const Ctx& c, Arena& ar, TT& t, const ttgbf_grid_cfg& g, const double* steps,
                            const int32_t* probes, int nprobes, ttgbf_diag* dg, double* sm) {
   const int d = t.d;
@@ -146,9 +147,9 @@ HDN int finalize_tt(const Ctx& c, Arena& ar, TT& t, const ttgbf_grid_cfg& g, con
     if (c.leader()) dg->mass_before_norm = mass;
     if (!isfinite(mass) || mass <= MASS_FLOOR) return E_DEGENERATE;
     tt_scale(c, t, 1.0 / mass);
-    CK(tt_round(c, ar, t, g.round_tol, g.round_max_rank, r, sm));
+    CK(tt_round(c, ar, t, g.round_tol, g.round_max_rank, r, sm, true));
   } else {
-    CK(tt_round(c, ar, t, g.round_tol, g.round_max_rank, r, sm));
+    CK(tt_round(c, ar, t, g.round_tol, g.round_max_rank, r, sm, true));
     const double mass = tt_sum(c, r, ws) * dv;
     if (c.leader()) dg->mass_before_norm = mass;
     if (!isfinite(mass) || mass <= MASS_FLOOR) return E_DEGENERATE;

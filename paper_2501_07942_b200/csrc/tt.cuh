@@ -181,39 +181,66 @@ HD void axis_cell(const AxisGeom& g, double x, int* cell, double* frac, bool* in
 // owns entries l, l+32, ... (S slots); v[a] is broadcast by shuffle and each
 // lane accumulates its output columns from coalesced core-row loads.
 template <int S, class Slice>
-__device__ __forceinline__ void chain_regs(const Ctx& c, const TT& t, int64_t K, Slice& slice, double* out) {
+__device__ __forceinline__ void chain_regs(const Ctx& c, const TT& t, int64_t K, Slice& s0, double* out) {
+  Slice s1 = s0;
   const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
-  for (int64_t p = warp; p < K; p += nwarps) {
-    double v[S];
+  for (int64_t p0 = 2 * (int64_t)warp; p0 < K; p0 += 2 * (int64_t)nwarps) {
+    const int64_t p1 = p0 + 1;
+    const bool has1 = p1 < K;
+    double v0[S], v1[S];
 #pragma unroll
-    for (int s = 0; s < S; ++s) v[s] = (s == 0 && lane == 0) ? 1.0 : 0.0;
-    bool dead = false;
+    for (int q = 0; q < S; ++q) { v0[q] = (q == 0 && lane == 0) ? 1.0 : 0.0; v1[q] = v0[q]; }
+    bool dead0 = false, dead1 = !has1;
     for (int k = 0; k < t.d; ++k) {
       const int rl = t.r[k], rr = t.r[k + 1];
-      if (!slice.prepare(k, p)) { dead = true; break; }
-      double acc[S];
+      const int64_t sa = (int64_t)t.n[k] * rr;
+      if (!dead0) dead0 = !s0.prepare(k, p0);
+      if (!dead1) dead1 = !s1.prepare(k, p1);
+      if (dead0 && dead1) break;
+      const double *lo0, *hi0, *lo1, *hi1;
+      double wl0, wh0, wl1, wh1;
+      s0.row(k, &lo0, &hi0, &wl0, &wh0);
+      if (has1) s1.row(k, &lo1, &hi1, &wl1, &wh1);
+      else { lo1 = lo0; hi1 = hi0; wl1 = wl0; wh1 = wh0; }
+      double a0[S], a1[S];
 #pragma unroll
-      for (int s = 0; s < S; ++s) acc[s] = 0.0;
+      for (int q = 0; q < S; ++q) { a0[q] = 0.0; a1[q] = 0.0; }
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        if (s * 32 < rl) {
-          const int amax = imin(32, rl - s * 32);
+      for (int sl = 0; sl < S; ++sl) {
+        if (sl * 32 < rl) {
+          const int amax = imin(32, rl - sl * 32);
+          const double* r0 = lo0 + (int64_t)(sl * 32) * sa + lane;
+          const double* r1 = lo1 + (int64_t)(sl * 32) * sa + lane;
+          const double* h0 = hi0 + (int64_t)(sl * 32) * sa + lane;
+          const double* h1 = hi1 + (int64_t)(sl * 32) * sa + lane;
           for (int l = 0; l < amax; ++l) {
-            const double va = __shfl_sync(0xffffffffu, v[s], l);
-            const int a = s * 32 + l;
+            const double va0 = __shfl_sync(0xffffffffu, v0[sl], l);
+            const double va1 = __shfl_sync(0xffffffffu, v1[sl], l);
 #pragma unroll
             for (int q = 0; q < S; ++q) {
-              const int b = q * 32 + lane;
-              if (b < rr) acc[q] = fma(va, slice.at(k, a, b), acc[q]);
+              if (q * 32 + lane < rr) {
+                double x0 = r0[q * 32], x1 = r1[q * 32];
+                if (Slice::kBlend) {
+                  x0 = x0 * wl0 + h0[q * 32] * wh0;
+                  x1 = x1 * wl1 + h1[q * 32] * wh1;
+                }
+                a0[q] = fma(va0, x0, a0[q]);
+                a1[q] = fma(va1, x1, a1[q]);
+              }
             }
+            r0 += sa; r1 += sa; h0 += sa; h1 += sa;
           }
         }
       }
 #pragma unroll
-      for (int s = 0; s < S; ++s) v[s] = acc[s];
+      for (int q = 0; q < S; ++q) { v0[q] = a0[q]; v1[q] = a1[q]; }
     }
-    const double r0 = __shfl_sync(0xffffffffu, v[0], 0);
-    if (lane == 0) out[p] = dead ? 0.0 : r0;
+    const double o0 = __shfl_sync(0xffffffffu, v0[0], 0);
+    const double o1 = __shfl_sync(0xffffffffu, v1[0], 0);
+    if (lane == 0) {
+      out[p0] = dead0 ? 0.0 : o0;
+      if (has1) out[p1] = dead1 ? 0.0 : o1;
+    }
   }
   c.sync();
 }
@@ -278,9 +305,16 @@ struct IndexSlice {
   const TT* t;
   const int32_t* idx;  // K x d
   int i;
+  static constexpr bool kBlend = false;
   HD bool prepare(int k, int64_t p) { i = idx[p * t->d + k]; return true; }
   HD double at(int k, int a, int b) const {
     return t->c[k][((int64_t)a * t->n[k] + i) * t->r[k + 1] + b];
+  }
+  HD void row(int k, const double** lo, const double** hi, double* wl, double* wh) const {
+    *lo = t->c[k] + (int64_t)i * t->r[k + 1];
+    *hi = *lo;
+    *wl = 1.0;
+    *wh = 0.0;
   }
 };
 
@@ -303,12 +337,26 @@ struct PointSlice {
     axis_cell(geo[k], pt(p, k), &cell, &frac, &inside);
     return inside;
   }
+  static constexpr bool kBlend = true;
   HD double at(int k, int a, int b) const {
     const int64_t rr = t->r[k + 1];
     const double* base = t->c[k] + ((int64_t)a * t->n[k] + cell) * rr + b;
     // lo * (1 - frac) + hi * frac, as tt_algorithms.py:741
     return base[0] * (1.0 - frac) + base[rr] * frac;
   }
+  HD void row(int k, const double** lo, const double** hi, double* wl, double* wh) const {
+    const int64_t rr = t->r[k + 1];
+    *lo = t->c[k] + (int64_t)cell * rr;
+    *hi = *lo + rr;
+    *wl = 1.0 - frac;
+    *wh = frac;
+  }
+};
+
+struct PtsFn {
+  const double* pts;
+  int d;
+  HD double operator()(int64_t p, int k) const { return pts[p * d + k]; }
 };
 
 // ---------------------------------------------------------------------------
@@ -697,16 +745,18 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
 // The result is written into `out` (allocated here, after the temporaries are
 // released, so the caller's arena holds only the output).
 // ---------------------------------------------------------------------------
-HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT& out, double* sm) {
+HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT& out, double* sm,
+                 bool destroy_input = false) {
   const int d = in.d;
   PROF(c, 7);
   if (d == 1) return tt_clone(c, ar, in, out);
   size_t mk0 = ar.mark();
   // Right-to-left: blocked Householder QR of core_k^T (rows (i, gamma), cols
   // alpha).  The reflectors stay in place (Q is never formed); R^T is carried
-  // into core k-1.
+  // into core k-1.  Temporaries are factored in place (no copy).
   TT w;
-  CK(tt_clone(c, ar, in, w));
+  if (destroy_input) w = in;
+  else CK(tt_clone(c, ar, in, w));
   double* taus[MAXD];
   double* Ts[MAXD];
   int mrow[MAXD], kq[MAXD];
@@ -983,7 +1033,7 @@ HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double to
     ar.release(mk);
   }
   TT R;
-  CK(tt_round(c, ar, P, tol, cap, R, sm));
+  CK(tt_round(c, ar, P, tol, cap, R, sm, true));
   // R sits after P in the arena: move it down over P
   ar.release(mk0);
   TT o;
