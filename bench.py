@@ -213,7 +213,8 @@ def run_ours(args):
     d = cfg["spec"]["F"].shape[0]
     b = np.atleast_2d(cfg["spec"]["R"]).shape[0]
     n = g["n_per_axis"]
-    runs = np.arange(rank * B, (rank + 1) * B)
+    from paper_2501_07942_b200.mc import shard
+    runs = shard(world * B, world, rank)          # weak scaling: B filters per GPU
     states, meas = trajectories(cfg, runs)
     kf = cfg["steps"]
     dev = torch.device("cuda", local)
@@ -254,12 +255,8 @@ def run_ours(args):
         i0, s0 = [int(v[0]) for v in np.nonzero(ok)]
         stats["ranks"] = {nm: [int(v) for v in recs[i0, s0]["ranks"][sl][: d + 1]]
                           for sl, nm in [(4, "kernel"), (5, "conv"), (6, "realign")]}
-    sq_err = np.zeros((B, d))
-    nerr = np.zeros(B)
-    for i, s_ in zip(*np.nonzero(ok)):
-        e = recs[i, s_]["mean"][:d] - states[i, recs[i, s_]["k"]]
-        sq_err[i] += e * e
-        nerr[i] += 1
+    from paper_2501_07942_b200.mc import gather_rmse, run_error_sums
+    local_err = run_error_sums(recs["mean"], states, recs["k"], ok, d)
     dev_s = sum(a.elapsed_time(e) / 1e3 for _, a, e in bank.timeline)
     per_kernel = {}
     for name, a, e in bank.timeline:
@@ -276,14 +273,9 @@ def run_ours(args):
         cc = torch.tensor([float(stats["completed"])], device=dev, dtype=torch.float64)
         dist.all_reduce(cc)
         done_all = int(cc[0])
-        # RMSE statistics: one NCCL all_gather of per-run sums
-        payload = torch.tensor(np.concatenate([sq_err, nerr[:, None]], axis=1), device=dev, dtype=torch.float64)
-        gathered = torch.empty((world * B, d + 1), device=dev, dtype=torch.float64)
-        dist.all_gather_into_tensor(gathered, payload)
-        allerr = gathered.cpu().numpy()
-    else:
-        allerr = np.concatenate([sq_err, nerr[:, None]], axis=1)
-    rmse = np.sqrt(allerr[:, :d].sum(0) / max(allerr[:, d].sum(), 1)).tolist()
+    # RMSE statistics: one NCCL all_gather of per-run sums, no other collective
+    rmse, _ = gather_rmse(local_err, device=dev if world > 1 else None)
+    rmse = rmse.tolist()
 
     if rank != 0:
         if world > 1:

@@ -225,6 +225,7 @@ def measurement_update(axes, cores, spec, z, cfg, cc, diag):
     res = _cross(shape, lambda idx: likelihood(spec, z, points_for(axes, idx)), cc,
                  seeds=seed_lattice(shape))
     _record(diag, "likelihood", res)
+    diag.setdefault("stage_lik", res.cores)
     prod = T.kron_cores(cores, res.cores)
     mass = T.total(prod) * cell_volume(axes)
     if not math.isfinite(mass) or mass <= MASS_FLOOR:
@@ -338,5 +339,6 @@ def step(axes, cores, spec, z, cfg, cc):
     _record(diag, "realign", rres)
     out = finalize(rres.cores, paxes, cfg, diag)
     diag["stages"] = {"kernel": kres.cores, "conv": conv, "shifted": shifted,
-                      "filt_cores": fcores, "realign": rres.cores, "faxes": faxes}
+                      "filt_cores": fcores, "realign": rres.cores, "faxes": faxes,
+                      "lik": diag.get("stage_lik"), "paxes": paxes}
     return paxes, out, diag
