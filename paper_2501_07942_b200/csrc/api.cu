@@ -319,8 +319,9 @@ extern "C" int ttgbf_test_draws(int kind, uint64_t* state6, const int* shape, in
   } else {
     std::vector<int32_t> disp(pop + 16, -1);
     std::vector<int64_t> touch(size + 16), draws(size + 16);
-    std::vector<uint64_t> gset(2 * (size + 16) + 64);
-    warp_choice(c, &g, &jt, pop, size, out, disp.data(), touch.data(), draws.data(),
+    std::vector<uint8_t> flags(size + 16);
+    std::vector<uint32_t> gset(4 * (size + 16) + 64);
+    warp_choice(c, &g, &jt, pop, size, out, disp.data(), touch.data(), draws.data(), flags.data(),
                 reinterpret_cast<uint32_t*>(smem.data() + SMEM_RED + SMEM_XBLK), 16384, gset.data(), &db);
     for (int64_t q = 0; q < pop; ++q)
       if (disp[q] != -1) return 99;   // displacement map must be restored

@@ -138,18 +138,25 @@ HDN void bitonic_sort(const Ctx& c, Key* a, int64_t P) {
 // [t*chunk, (t+1)*chunk); returns this thread's output offset and the total.
 HDN int64_t scan_offsets(const Ctx& c, int64_t mine, int64_t* total) {
 #if ENGINE_DEVICE
-  int64_t* buf = reinterpret_cast<int64_t*>(c.red) + 64;   // needs nt int64 after red[0..64)
+  // exclusive block scan: warp inclusive scan by shuffles, then warp totals
+  const int lane = c.tid & 31, w = c.tid >> 5, nw = (c.nt + 31) >> 5;
+  int64_t* wt = reinterpret_cast<int64_t*>(c.red) + 64;   // nw warp totals
+  int64_t x = mine;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
   __syncthreads();
-  buf[c.tid] = mine;
+  if (lane == 31) wt[w] = x;
   __syncthreads();
-  int64_t off = 0, tot = 0;
-  for (int t = 0; t < c.nt; ++t) {
-    if (t < c.tid) off += buf[t];
-    tot += buf[t];
+  int64_t base = 0, tot = 0;
+  for (int i = 0; i < nw; ++i) {
+    if (i < w) base += wt[i];
+    tot += wt[i];
   }
   __syncthreads();
   *total = tot;
-  return off;
+  return base + x - mine;
 #else
   (void)c;
   *total = mine;

@@ -62,7 +62,8 @@ struct XShared {           // leader-published scalars
 
 struct ChoiceWs {
   int32_t* disp;     // virtual arange for tail shuffles (-1 = untouched)
-  uint64_t* gset;    // Floyd set when it does not fit shared memory
+  uint32_t* gset;    // Floyd first-occurrence table when it does not fit shared memory
+  uint8_t* flags;    // per-draw collision flags
   int64_t* touch;    // touched positions / shuffle draws
   int64_t* draws;    // pre-drawn bounded values
   const PcgJump* jt; // PCG64 jump-ahead table of this stream
@@ -324,8 +325,8 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
   ALLOC(e, double, X_SCAN, ar);
   {
     PROF(c, 10);
-    warp_choice(c, &sh->rng, rws.jt, g.nrow, qr, cr, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
-    warp_choice(c, &sh->rng, rws.jt, g.ncol, qc, cc, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, g.nrow, qr, cr, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, g.ncol, qc, cc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
   }
   if (c.leader()) {
     for (int i = 0; i < qr; ++i)
@@ -362,7 +363,7 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
     int nsr = 0;
     if (g.nrow > X_SCAN) {
       PROF(c, 10);
-      warp_choice(c, &sh->rng, rws.jt, g.nrow, X_SCAN, br, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+      warp_choice(c, &sh->rng, rws.jt, g.nrow, X_SCAN, br, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
     }
     if (c.leader()) {
       if (g.nrow > X_SCAN) nsr = X_SCAN;
@@ -382,7 +383,7 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
     int nsc = 0;
     if (g.ncol > X_SCAN) {
       PROF(c, 10);
-      warp_choice(c, &sh->rng, rws.jt, g.ncol, X_SCAN, bc, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+      warp_choice(c, &sh->rng, rws.jt, g.ncol, X_SCAN, bc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
     }
     if (c.leader()) {
       if (g.ncol > X_SCAN) nsc = X_SCAN;
@@ -444,7 +445,7 @@ HDN int x_check(const Ctx& c, Arena& ar, Cache* C, XShared* sh, const ChoiceWs& 
   ALLOC(tv, double, K, ar);
   if (cnt > count) {
     PROF(c, 10);
-    warp_choice(c, &sh->rng, rws.jt, cnt, count, sel, rws.disp, rws.touch, rws.draws, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, cnt, count, sel, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
   } else if (c.leader()) {
     for (int64_t i = 0; i < cnt; ++i) sel[i] = i;
   }
@@ -546,7 +547,8 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
     int maxn = 1;
     for (int k = 0; k < d; ++k) maxn = imax(maxn, spec.n[k]);
     const int64_t dcap = lmax(cfg.cache_cap + 16, (int64_t)cfg.max_rank * maxn + 16);
-    ALLOC(rws.gset, uint64_t, gen_mask((uint64_t)(1.2 * X_GATE)) + 1, ar);
+    ALLOC(rws.gset, uint32_t, 2 * (gen_mask((uint64_t)(1.2 * X_GATE)) + 1), ar);
+    ALLOC(rws.flags, uint8_t, X_GATE + X_SCAN, ar);
     ALLOC(rws.disp, int32_t, dcap, ar);
     ALLOC(rws.touch, int64_t, X_GATE + X_SCAN, ar);
     ALLOC(rws.draws, int64_t, X_GATE + X_SCAN, ar);

@@ -253,148 +253,164 @@ HDN void warp_integers(const Ctx& c, Pcg64* g, const PcgJump* jt, const int* sha
   c.sync();
 }
 
+// Warp-batched resolution of a Fisher-Yates swap sequence: step t swaps
+// positions I(t) > ... (decreasing) and J(t) <= I(t).  Values of untouched
+// positions come from get(pos); set(pos, v) writes; fin(t, pos_i, v) receives
+// the final value of position I(t) (never touched again).  Lanes load the 32
+// steps' operands at once; in-batch dependencies are resolved by shuffles.
+template <class IFn, class JFn, class Get, class Set, class Fin>
+HD void swap_resolve(const Ctx& c, int64_t ns, IFn I, JFn J, Get get, Set set, Fin fin) {
+  const bool w0 = !ENGINE_DEVICE || c.tid < 32;
+  if (!w0) return;
+  for (int64_t t0 = 0; t0 < ns; t0 += 32) {
+    const int m = (int)lmin(32, ns - t0);
+#if ENGINE_DEVICE
+    const int l = c.tid & 31;
+    const bool act = l < m;
+    const int64_t i = act ? I(t0 + l) : -1;
+    const int64_t j = act ? J(t0 + l) : -2;
+    const int64_t ldj = act ? get(j) : 0;
+    const int64_t ldi = act ? get(i) : 0;
+    int wj = -1, wi = -1, later = 0;
+    for (int q = 0; q < 32; ++q) {
+      const int64_t jq = __shfl_sync(0xffffffffu, j, q);
+      if (q < l && q < m) {
+        if (jq == j) wj = q;
+        if (jq == i) wi = q;
+      }
+      if (q > l && q < m && jq == j) later = 1;
+    }
+    int64_t vi = ldi;
+    for (int it = 0; it < 32; ++it) {
+      const int64_t src = __shfl_sync(0xffffffffu, vi, wi < 0 ? l : wi);
+      const int64_t nv = wi < 0 ? ldi : src;
+      const bool ch = nv != vi;
+      vi = nv;
+      if (!__any_sync(0xffffffffu, ch)) break;
+    }
+    const int64_t viw = __shfl_sync(0xffffffffu, vi, wj < 0 ? l : wj);
+    const int64_t vj = wj < 0 ? ldj : viw;
+    if (act) {
+      if (!later) set(j, vi);
+      fin(t0 + l, i, vj);
+    }
+    __syncwarp();
+#else
+    int64_t Iv[32], Jv[32], VI[32], LDJ[32], LDI[32];
+    for (int l = 0; l < m; ++l) {
+      Iv[l] = I(t0 + l);
+      Jv[l] = J(t0 + l);
+      LDJ[l] = get(Jv[l]);
+      LDI[l] = get(Iv[l]);
+    }
+    for (int l = 0; l < m; ++l) {
+      int wi = -1;
+      for (int q = 0; q < l; ++q) if (Jv[q] == Iv[l]) wi = q;
+      VI[l] = wi < 0 ? LDI[l] : VI[wi];
+    }
+    for (int l = 0; l < m; ++l) {
+      int wj = -1, later = 0;
+      for (int q = 0; q < l; ++q) if (Jv[q] == Jv[l]) wj = q;
+      for (int q = l + 1; q < m; ++q) if (Jv[q] == Jv[l]) later = 1;
+      const int64_t vj = wj < 0 ? LDJ[l] : VI[wj];
+      if (!later) set(Jv[l], VI[l]);
+      fin(t0 + l, Iv[l], vj);
+    }
+#endif
+  }
+}
+
 // rng.choice(pop, size, replace=False) with pre-drawn bounds.
-// disp: >= pop int32 all -1 (restored); touch: >= size int64; draws: >= size int64;
-// sset: shared scratch (>= 64 KB) for Floyd's set + the result when they fit.
+// disp: >= pop int32 all -1 (restored); touch, draws: >= size int64;
+// flags: >= size bytes; sset: shared scratch (sset_words32 uint32);
+// gset: global scratch >= 2*(gen_mask(1.2*size)+1) uint32.
 HDN void warp_choice(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t pop, int64_t size, int64_t* out,
-                     int32_t* disp, int64_t* touch, int64_t* draws, uint32_t* sset, int64_t sset_words32,
-                     uint64_t* gset, DrawBuf* db) {
+                     int32_t* disp, int64_t* touch, int64_t* draws, uint8_t* flags, uint32_t* sset,
+                     int64_t sset_words32, uint32_t* gset, DrawBuf* db) {
   if (pop > 10000 && size > pop / 50) {
     int64_t first = pop - size;
     if (first < 1) first = 1;
     const int64_t ns = pop - first;
     warp_draws(c, g, jt, ns, BoundDown{pop - 1}, draws, db);   // draw t: j for i = pop-1-t
-    const bool w0 = !ENGINE_DEVICE || c.tid < 32;
-    if (w0) {
-      for (int64_t t0 = 0; t0 < ns; t0 += 32) {
-        const int m = (int)lmin(32, ns - t0);
-#if ENGINE_DEVICE
-        {
-          const int l = c.tid & 31;
-          const bool act = l < m;
-          const int64_t i = act ? pop - 1 - (t0 + l) : -1;
-          const int64_t j = act ? draws[t0 + l] : -2;
-          const int ldj = act ? disp[j] : -1;
-          const int ldi = act ? disp[i] : -1;
-          int wj = -1, wi = -1, later = 0;
-          for (int q = 0; q < 32; ++q) {
-            const int64_t jq = __shfl_sync(0xffffffffu, j, q);
-            if (q < l && q < m) {
-              if (jq == j) wj = q;
-              if (jq == i) wi = q;
-            }
-            if (q > l && q < m && jq == j) later = 1;
-          }
-          int64_t vi0 = ldi < 0 ? i : (int64_t)ldi;
-          int64_t vi = vi0;
-          for (int it = 0; it < 32; ++it) {
-            const int64_t src = __shfl_sync(0xffffffffu, vi, wi < 0 ? l : wi);
-            const int64_t nv = wi < 0 ? vi0 : src;
-            const bool ch = nv != vi;
-            vi = nv;
-            if (!__any_sync(0xffffffffu, ch)) break;
-          }
-          const int64_t viw = __shfl_sync(0xffffffffu, vi, wj < 0 ? l : wj);
-          const int64_t vj = wj < 0 ? (ldj < 0 ? j : (int64_t)ldj) : viw;
-          if (act) {
-            if (!later) disp[j] = (int32_t)vi;
-            if (i >= pop - size) out[i - (pop - size)] = vj;
-            touch[t0 + l] = j;
-          }
-          __syncwarp();
-        }
-#else
-        {
-          int64_t I[32], J[32], VI[32];
-          int LDJ[32], LDI[32];
-          for (int l = 0; l < m; ++l) {
-            I[l] = pop - 1 - (t0 + l);
-            J[l] = draws[t0 + l];
-            LDJ[l] = disp[J[l]];
-            LDI[l] = disp[I[l]];
-          }
-          for (int l = 0; l < m; ++l) {
-            int wi = -1;
-            for (int q = 0; q < l; ++q) if (J[q] == I[l]) wi = q;
-            VI[l] = wi < 0 ? (LDI[l] < 0 ? I[l] : LDI[l]) : VI[wi];
-          }
-          for (int l = 0; l < m; ++l) {
-            int wj = -1, later = 0;
-            for (int q = 0; q < l; ++q) if (J[q] == J[l]) wj = q;
-            for (int q = l + 1; q < m; ++q) if (J[q] == J[l]) later = 1;
-            const int64_t vj = wj < 0 ? (LDJ[l] < 0 ? J[l] : LDJ[l]) : VI[wj];
-            if (!later) disp[J[l]] = (int32_t)VI[l];
-            if (I[l] >= pop - size) out[I[l] - (pop - size)] = vj;
-            touch[t0 + l] = J[l];
-          }
-        }
-#endif
-      }
-    }
+    const int64_t lo = pop - size;
+    swap_resolve(
+        c, ns, [=](int64_t t) { return pop - 1 - t; }, [=](int64_t t) { return draws[t]; },
+        [=](int64_t pos) { const int32_t v = disp[pos]; return v < 0 ? pos : (int64_t)v; },
+        [=](int64_t pos, int64_t v) { disp[pos] = (int32_t)v; },
+        [=](int64_t t, int64_t pos, int64_t v) {
+          if (pos >= lo) out[pos - lo] = v;
+          touch[t] = draws[t];
+        });
     c.sync();
     for (int64_t q = c.tid; q < ns; q += c.nt) disp[touch[q]] = -1;
     c.sync();
     return;
   }
-  // Floyd: draws for j = pop-size..pop-1, then the shuffle draws for i = size-1..1
+  // Floyd: draws val_t for j_t = pop-size+t, then the shuffle draws (i = size-1..1)
   warp_draws(c, g, jt, size, BoundUp{pop - size}, draws, db);
-  const uint64_t mask = gen_mask((uint64_t)(1.2 * (double)size));
-  const bool small = (int64_t)(mask + 1) + 2 * size <= sset_words32;
-  int64_t* sdraws = touch;   // reuse: shuffle draws
+  int64_t* sdraws = touch;
   warp_draws(c, g, jt, size > 1 ? size - 1 : 0, BoundDown{size - 1}, sdraws, db);
+  // first occurrence of each value: open addressing, key = value, payload = min t
+  const uint64_t mask = gen_mask((uint64_t)(1.2 * (double)size));
+  const int64_t tsz = (int64_t)mask + 1;
+  uint32_t* keys = (2 * tsz <= sset_words32) ? sset : gset;
+  uint32_t* mins = keys + tsz;
+  for (int64_t q = c.tid; q < tsz; q += c.nt) { keys[q] = 0xFFFFFFFFu; mins[q] = 0xFFFFFFFFu; }
+  c.sync();
+  for (int64_t t = c.tid; t < size; t += c.nt) {
+    const uint32_t v = (uint32_t)draws[t];
+    uint64_t h = v & mask;
+    while (true) {
+#if ENGINE_DEVICE
+      const uint32_t old = atomicCAS(&keys[h], 0xFFFFFFFFu, v);
+      if (old == 0xFFFFFFFFu || old == v) { atomicMin(&mins[h], (uint32_t)t); break; }
+#else
+      if (keys[h] == 0xFFFFFFFFu || keys[h] == v) {
+        keys[h] = v;
+        if ((uint32_t)t < mins[h]) mins[h] = (uint32_t)t;
+        break;
+      }
+#endif
+      h = (h + 1) & mask;
+    }
+  }
+  c.sync();
+  // provisional outputs; flag steps that may collide (duplicate value or a
+  // value in the j-range pop-size..)
+  const int64_t jlo = pop - size;
+  for (int64_t t = c.tid; t < size; t += c.nt) {
+    const uint32_t v = (uint32_t)draws[t];
+    uint64_t h = v & mask;
+    while (keys[h] != v) h = (h + 1) & mask;
+    const bool rare = mins[h] < (uint32_t)t || (int64_t)v >= jlo;
+    flags[t] = rare ? 2 : 0;
+    out[t] = (int64_t)v;
+  }
+  c.sync();
+  // in-order resolution of the rare steps (leader): collided[t] lives in flags bit 0
   if (c.leader()) {
-    uint32_t* hs32 = sset;
-    int32_t* res = reinterpret_cast<int32_t*>(sset + (mask + 1));
-    if (small) {
-      for (uint64_t q = 0; q <= mask; ++q) hs32[q] = 0xFFFFFFFFu;
-      for (int64_t t = 0; t < size; ++t) {
-        const int64_t j = pop - size + t;
-        const uint32_t val = (uint32_t)draws[t];
-        uint64_t loc = val & mask;
-        while (hs32[loc] != 0xFFFFFFFFu && hs32[loc] != val) loc = (loc + 1) & mask;
-        if (hs32[loc] == 0xFFFFFFFFu) {
-          hs32[loc] = val;
-          res[t] = (int32_t)val;
-        } else {
-          loc = (uint64_t)j & mask;
-          while (hs32[loc] != 0xFFFFFFFFu) loc = (loc + 1) & mask;
-          hs32[loc] = (uint32_t)j;
-          res[t] = (int32_t)j;
-        }
+    for (int64_t t = 0; t < size; ++t) {
+      if (!(flags[t] & 2)) continue;
+      const uint32_t v = (uint32_t)draws[t];
+      uint64_t h = v & mask;
+      while (keys[h] != v) h = (h + 1) & mask;
+      bool coll = mins[h] < (uint32_t)t;
+      if (!coll && (int64_t)v >= jlo) {
+        const int64_t sidx = (int64_t)v - jlo;
+        coll = sidx < t && (flags[sidx] & 1);
       }
-      for (int64_t q = 0; q < size - 1; ++q) {
-        const int64_t i = size - 1 - q, j = sdraws[q];
-        const int32_t tt = res[j];
-        res[j] = res[i];
-        res[i] = tt;
-      }
-      for (int64_t t = 0; t < size; ++t) out[t] = res[t];
-    } else {
-      uint64_t* hs = gset;
-      for (uint64_t q = 0; q <= mask; ++q) hs[q] = ~0ull;
-      for (int64_t t = 0; t < size; ++t) {
-        const int64_t j = pop - size + t;
-        const uint64_t val = (uint64_t)draws[t];
-        uint64_t loc = val & mask;
-        while (hs[loc] != ~0ull && hs[loc] != val) loc = (loc + 1) & mask;
-        if (hs[loc] == ~0ull) {
-          hs[loc] = val;
-          out[t] = (int64_t)val;
-        } else {
-          loc = (uint64_t)j & mask;
-          while (hs[loc] != ~0ull) loc = (loc + 1) & mask;
-          hs[loc] = (uint64_t)j;
-          out[t] = j;
-        }
-      }
-      for (int64_t q = 0; q < size - 1; ++q) {
-        const int64_t i = size - 1 - q, j = sdraws[q];
-        const int64_t tt = out[j];
-        out[j] = out[i];
-        out[i] = tt;
+      if (coll) {
+        out[t] = jlo + t;
+        flags[t] |= 1;
       }
     }
   }
+  c.sync();
+  // Fisher-Yates shuffle of out[0..size): step q swaps i = size-1-q and j = sdraws[q]
+  swap_resolve(
+      c, size > 1 ? size - 1 : 0, [=](int64_t q) { return size - 1 - q; }, [=](int64_t q) { return sdraws[q]; },
+      [=](int64_t pos) { return out[pos]; }, [=](int64_t pos, int64_t v) { out[pos] = v; },
+      [=](int64_t, int64_t pos, int64_t v) { out[pos] = v; });
   c.sync();
 }
 

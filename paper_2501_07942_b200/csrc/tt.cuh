@@ -213,6 +213,7 @@ __device__ __forceinline__ void chain_regs(const Ctx& c, const TT& t, int64_t K,
           const double* r1 = lo1 + (int64_t)(sl * 32) * sa + lane;
           const double* h0 = hi0 + (int64_t)(sl * 32) * sa + lane;
           const double* h1 = hi1 + (int64_t)(sl * 32) * sa + lane;
+#pragma unroll 4
           for (int l = 0; l < amax; ++l) {
             const double va0 = __shfl_sync(0xffffffffu, v0[sl], l);
             const double va1 = __shfl_sync(0xffffffffu, v1[sl], l);

@@ -48,7 +48,8 @@ def test_integers_match_numpy(lib, seed):
 
 
 @pytest.mark.parametrize("pop,size", [(5, 3), (33, 10), (1000, 10), (5000, 1024), (9999, 4096), (10001, 1024),
-                                      (20000, 4096), (300000, 4096), (150000, 32768), (12000, 32768 // 4)])
+                                      (20000, 4096), (300000, 4096), (150000, 32768), (12000, 32768 // 4),
+                                      (1030, 1024), (2049, 2048), (4097, 4096), (2000000, 32768)])
 def test_choice_matches_numpy(lib, pop, size):
     for seed in range(3):
         rng = np.random.default_rng(seed)
