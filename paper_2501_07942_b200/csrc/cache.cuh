@@ -242,7 +242,7 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
       for (int64_t e = c.tid; e < M * d; e += c.nt) coords[e] = realign_coord(spec, uidx + (e / d) * d, (int)(e % d));
       c.sync();
       PointSlice<PtsFn> ps{&spec.conv, spec.geo, PtsFn{coords, d}, 0, 0.0};
-      tt_chain_eval(c, spec.conv, M, ps, nv, sm);
+      CK(tt_eval_bucketed(c, ar, spec.conv, M, ps, nv, sm));
     } else {
       for (int64_t j = c.tid; j < M; j += c.nt) nv[j] = eval_point(spec, uidx + j * d);
     }

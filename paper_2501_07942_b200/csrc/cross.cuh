@@ -455,7 +455,11 @@ HDN int x_check(const Ctx& c, Arena& ar, Cache* C, XShared* sh, const ChoiceWs& 
     vals[p] = C->vals[sel[p]];
   }
   c.sync();
-  { PROF(c, 12); tt_eval_idx(c, t, idx, K, tv, sm); }
+  {
+    PROF(c, 12);
+    IndexSlice is{&t, idx, 0};
+    CK(tt_eval_bucketed(c, ar, t, K, is, tv, sm));
+  }
   for (int64_t p = c.tid; p < K; p += c.nt) tv[p] = fabs(vals[p] - tv[p]);
   c.sync();
   // top-k: repeated arg-max preferring the LAST index on ties (argsort[::-1])

@@ -317,6 +317,12 @@ struct IndexSlice {
     *wl = 1.0;
     *wh = 0.0;
   }
+  HD bool locate(int k, int64_t p, int* s, double* wl, double* wh) const {
+    *s = idx[p * t->d + k];
+    *wl = 1.0;
+    *wh = 0.0;
+    return true;
+  }
 };
 
 HDN void tt_eval_idx(const Ctx& c, const TT& t, const int32_t* idx, int64_t K, double* out, double* sm) {
@@ -352,6 +358,16 @@ struct PointSlice {
     *wl = 1.0 - frac;
     *wh = frac;
   }
+  HD bool locate(int k, int64_t p, int* s, double* wl, double* wh) const {
+    int cl;
+    double fr;
+    bool inside;
+    axis_cell(geo[k], pt(p, k), &cl, &fr, &inside);
+    *s = cl;
+    *wl = 1.0 - fr;
+    *wh = fr;
+    return inside;
+  }
 };
 
 struct PtsFn {
@@ -359,6 +375,184 @@ struct PtsFn {
   int d;
   HD double operator()(int64_t p, int k) const { return pts[p * d + k]; }
 };
+
+// ---------------------------------------------------------------------------
+// Core-major TT evaluation for large batches: for each core the points are
+// bucketed by their slice (counting sort), each slice (and its right
+// neighbour for 2-tap interpolation) is staged in SMEM, and one warp
+// advances two points at a time reading the core from SMEM instead of L2.
+// Same arithmetic order as tt_chain_eval (blend, then sum over a ascending).
+// Falls back to tt_chain_eval for small batches or ranks > 64.
+// ---------------------------------------------------------------------------
+constexpr int64_t BUCKET_MIN_K = 2048;
+
+template <class Slice>
+HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice slice, double* out, double* sm) {
+  int maxr = 1, maxn = 1;
+  for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
+  for (int k = 0; k < t.d; ++k) maxn = imax(maxn, t.n[k]);
+  if (maxr > 60 || K < BUCKET_MIN_K || maxn > 1000) {
+    tt_chain_eval(c, t, K, slice, out, sm);
+    return OK;
+  }
+  const int d = t.d;
+  const size_t mk = ar.mark();
+  double *V0, *V1, *wlv, *whv;
+  int32_t *sid, *perm, *offs;
+  uint8_t* dead;
+  ALLOC(V0, double, K * maxr, ar);
+  ALLOC(V1, double, K * maxr, ar);
+  ALLOC(wlv, double, K, ar);
+  ALLOC(whv, double, K, ar);
+  ALLOC(sid, int32_t, K, ar);
+  ALLOC(perm, int32_t, K, ar);
+  ALLOC(offs, int32_t, maxn + 2, ar);
+  ALLOC(dead, uint8_t, K, ar);
+  // core 0 (left rank 1): V0[p, b] = blended slice row
+  {
+    const int r1 = t.r[1], n0 = t.n[0];
+    (void)n0;
+    for (int64_t p = c.tid; p < K; p += c.nt) {
+      int sl;
+      double wl, wh;
+      const bool in = slice.locate(0, p, &sl, &wl, &wh);
+      dead[p] = in ? 0 : 1;
+      const double* lo = t.c[0] + (int64_t)sl * r1;
+      for (int b = 0; b < r1; ++b) {
+        double x = lo[b];
+        if (Slice::kBlend) x = x * wl + lo[r1 + b] * wh;
+        V0[p * maxr + b] = x;
+      }
+    }
+  }
+  c.sync();
+  double* Vin = V0;
+  double* Vout = V1;
+  int* cur = reinterpret_cast<int*>(sm);          // bucket cursors (maxn + 1 <= 1001 ints)
+  double* A = sm + 512;                          // slice s   (rl x rr <= 60 x 60)
+  double* B = A + 60 * 60;                       // slice s+1 (interpolation); ends at 7712 doubles
+  for (int k = 1; k < d; ++k) {
+    const int rl = t.r[k], rr = t.r[k + 1], n = t.n[k];
+    for (int q = c.tid; q <= n; q += c.nt) cur[q] = 0;
+    c.sync();
+    for (int64_t p = c.tid; p < K; p += c.nt) {
+      int sl;
+      double wl, wh;
+      const bool in = slice.locate(k, p, &sl, &wl, &wh);
+      if (!in) dead[p] = 1;
+      sid[p] = sl;
+      wlv[p] = wl;
+      whv[p] = wh;
+#if ENGINE_DEVICE
+      atomicAdd(&cur[sl], 1);
+#else
+      cur[sl] += 1;
+#endif
+    }
+    c.sync();
+    if (c.leader()) {
+      int acc = 0;
+      for (int q = 0; q < n; ++q) { offs[q] = acc; const int h = cur[q]; cur[q] = acc; acc += h; }
+      offs[n] = acc;
+    }
+    c.sync();
+    for (int64_t p = c.tid; p < K; p += c.nt) {
+#if ENGINE_DEVICE
+      const int pos = atomicAdd(&cur[sid[p]], 1);
+#else
+      const int pos = cur[sid[p]]++;
+#endif
+      perm[pos] = (int32_t)p;
+    }
+    c.sync();
+    const double* G = t.c[k];
+    const int64_t sa = (int64_t)n * rr;
+    for (int sl = 0; sl < n; ++sl) {
+      const int beg = offs[sl], end = offs[sl + 1];
+      if (beg == end) continue;
+      for (int e = c.tid; e < rl * rr; e += c.nt) {
+        const int a = e / rr, bb = e % rr;
+        A[e] = G[a * sa + (int64_t)sl * rr + bb];
+        if (Slice::kBlend) B[e] = (sl + 1 < n) ? G[a * sa + (int64_t)(sl + 1) * rr + bb] : 0.0;
+      }
+      c.sync();
+#if ENGINE_DEVICE
+      {
+        const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
+        for (int q0 = beg + 2 * warp; q0 < end; q0 += 2 * nwarps) {
+          const bool has1 = q0 + 1 < end;
+          const int p0 = perm[q0], p1 = has1 ? perm[q0 + 1] : p0;
+          const double wl0 = wlv[p0], wh0 = whv[p0], wl1 = wlv[p1], wh1 = whv[p1];
+          double v0[2], v1[2], a0[2], a1[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int a = h * 32 + lane;
+            v0[h] = a < rl ? Vin[(int64_t)p0 * maxr + a] : 0.0;
+            v1[h] = a < rl ? Vin[(int64_t)p1 * maxr + a] : 0.0;
+            a0[h] = 0.0;
+            a1[h] = 0.0;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (h * 32 < rl) {
+              const int amax = imin(32, rl - h * 32);
+#pragma unroll 4
+              for (int l = 0; l < amax; ++l) {
+                const double va0 = __shfl_sync(0xffffffffu, v0[h], l);
+                const double va1 = __shfl_sync(0xffffffffu, v1[h], l);
+                const int a = h * 32 + l;
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                  const int bb = q * 32 + lane;
+                  if (bb < rr) {
+                    const double xa = A[a * rr + bb];
+                    double x0 = xa, x1 = xa;
+                    if (Slice::kBlend) {
+                      const double xb = B[a * rr + bb];
+                      x0 = xa * wl0 + xb * wh0;
+                      x1 = xa * wl1 + xb * wh1;
+                    }
+                    a0[q] = fma(va0, x0, a0[q]);
+                    a1[q] = fma(va1, x1, a1[q]);
+                  }
+                }
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int bb = q * 32 + lane;
+            if (bb < rr) {
+              Vout[(int64_t)p0 * maxr + bb] = a0[q];
+              if (has1) Vout[(int64_t)p1 * maxr + bb] = a1[q];
+            }
+          }
+        }
+      }
+#else
+      for (int q0 = beg; q0 < end; ++q0) {
+        const int p = perm[q0];
+        const double wl = wlv[p], wh = whv[p];
+        for (int bb = 0; bb < rr; ++bb) {
+          double acc = 0.0;
+          for (int a = 0; a < rl; ++a) {
+            double x = A[a * rr + bb];
+            if (Slice::kBlend) x = x * wl + B[a * rr + bb] * wh;
+            acc = fma(Vin[(int64_t)p * maxr + a], x, acc);
+          }
+          Vout[(int64_t)p * maxr + bb] = acc;
+        }
+      }
+#endif
+      c.sync();
+    }
+    double* tmp = Vin; Vin = Vout; Vout = tmp;
+  }
+  for (int64_t p = c.tid; p < K; p += c.nt) out[p] = dead[p] ? 0.0 : Vin[p * maxr];
+  c.sync();
+  ar.release(mk);
+  return OK;
+}
 
 // ---------------------------------------------------------------------------
 // Hadamard product cores (tensor_train.py:252-266)
@@ -1090,7 +1284,8 @@ HDN int tt_negative_mass(const Ctx& c, Arena& ar, const TT& t, int64_t guard, co
   } else {
     double* vals;
     ALLOC(vals, double, nprobes, ar);
-    tt_eval_idx(c, t, probes, nprobes, vals, sm);
+    IndexSlice is{&t, probes, 0};
+    CK(tt_eval_bucketed(c, ar, t, nprobes, is, vals, sm));
     double part = 0.0;
     for (int e = c.tid; e < nprobes; e += c.nt) part += fmax(-vals[e], 0.0);
     *result = block_sum(c, part) / (double)nprobes * (double)total;
