@@ -242,8 +242,13 @@ def run_ours(args):
     stats["completed"] = int(ok.sum())
     stats["failed"] = int((recs["status"] > 0).sum())
     stats["restarts"] = int((recs["status"] != 0).sum())
+    step_fl = []
     for i, s_ in zip(*np.nonzero(recs["status"] >= 0)):
-        stats["flops"] += sum(rl.rec_flops(recs[i, s_], d, b, n))
+        fl = sum(rl.rec_flops(recs[i, s_], d, b, n))
+        stats["flops"] += fl
+        step_fl.append(fl)
+    step_fl = np.array(step_fl) if step_fl else np.zeros(1)
+    stats["step_gflop_pcts"] = [round(float(np.percentile(step_fl, q)) / 1e9, 3) for q in (50, 90, 99, 100)]
     stats["cycles"] = dg["cycles"].sum(axis=0).astype(float)
     stats["prof"] = dg["prof"].sum(axis=0).astype(float)
     stats["ws_peak"] = int(dg["ws_peak"].max())
@@ -309,6 +314,7 @@ def run_ours(args):
         "completed_frac": stats["completed"] / max(1, B * args.steps),
         "ws_peak_mb": stats["ws_peak"] / 2 ** 20,
         "mean_cross_calls": stats["calls"],
+        "step_gflop_p50_p90_p99_max": stats["step_gflop_pcts"],
         "stage_sm_seconds_per_attempted_step": stats["stage_s_per_step"],
         "example_ranks": stats["ranks"],
         "rmse": rmse,

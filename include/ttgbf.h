@@ -193,14 +193,15 @@ typedef struct {
 
 /* io[f].active is the filter's alive flag and io[f].cur its grid (in/out);
  * kstep[f] its trajectory position (in/out); Z: nfilt x kf x b measurements;
- * rec: nfilt x steps records.  Workspace is a pool of `nslots` slots of
- * ws_bytes (slot_busy: nslots int32, zero-initialised); each CTA claims a free
- * slot for its lifetime, so nfilt may exceed the number of resident CTAs and
- * the block scheduler balances filters of very different cost. */
+ * rec: nfilt x steps records.  Scheduling is per STEP: `nslots` persistent
+ * CTAs (one per workspace slot of ws_bytes) repeatedly claim any filter that
+ * still has steps to run (per-filter lock), run one step and release it, so
+ * filters whose steps cost 10x more than others do not leave SMs idle.
+ * sched: 2 + 2*nfilt int32, zero-initialised (cursor, done, locks, counts). */
 int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
                      ttgbf_run_cfg rcfg, ttgbf_filter_io* io, int32_t* kstep, const double* Z, int nfilt,
                      const int32_t* probes, int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr,
-                     double* state, int64_t state_cap, void* ws, int64_t ws_bytes, int32_t* slot_busy,
+                     double* state, int64_t state_cap, void* ws, int64_t ws_bytes, int32_t* sched,
                      int nslots, ttgbf_diag* diag, ttgbf_step_rec* rec, void* stream);
 
 /* ---- filter stages: one CTA per filter, nfilt filters per launch ---------

@@ -160,7 +160,7 @@ class FilterBank:
         self.state = backend.empty(n * cfg.state_doubles * 8)
         self.nslots = min(n, cfg.ws_slots) if cfg.ws_slots > 0 else n
         self.ws = backend.empty(self.nslots * cfg.ws_bytes)
-        self.slot_busy = backend.upload(np.zeros(max(1, self.nslots), dtype=np.int32))
+        self.sched = backend.empty(4 * (2 + 2 * n))
         self.diag_dev = backend.empty(n * _abi.DIAG.itemsize)
         self.grids: list[geo.Axes | None] = [None] * n
         self.alive = np.zeros(n, dtype=bool)
@@ -328,6 +328,8 @@ class FilterBank:
             rc.prior_grid[k].step = float(dev["step"][k])
             rc.prior_grid[k].off = int(dev["off"][k])
             rc.prior_grid[k].n = int(dev["n"][k])
+        self.be.zero(self.sched)
+        self.be.zero(self.diag_dev)
         zb = self.be.upload(Z)
         self.bytes_h2d += Z.nbytes
         rec = self.be.empty(self.count * max(1, steps) * _abi.STEP_REC.itemsize)
@@ -337,7 +339,7 @@ class FilterBank:
         self._launch("ttgbf_filter_run", self.lib.ttgbf_filter_run, self.model.ptr, prior_dev.ptr, self.gcfg,
                      self.xcfg, rc, self.io_dev.ptr, self.kstep_dev.ptr, zb.ptr, self.count, pr, npr, sd, nsd,
                      self.hdr.ptr, self.state.ptr, self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes,
-                     self.slot_busy.ptr, self.nslots, self.diag_dev.ptr, rec.ptr, self.be.stream_ptr)
+                     self.sched.ptr, self.nslots, self.diag_dev.ptr, rec.ptr, self.be.stream_ptr)
         recs = self.be.download(rec, _abi.STEP_REC, self.count * steps).reshape(self.count, steps)
         self.io = self.be.download(self.io_dev, _abi.FILTER_IO, self.count)
         self.bytes_d2h += recs.nbytes + self.io.nbytes

@@ -137,45 +137,73 @@ int ttgbf_filter_time_update(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgb
 int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
                      ttgbf_run_cfg rcfg, ttgbf_filter_io* io, int32_t* kstep, const double* Z, int nfilt,
                      const int32_t* probes, int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr,
-                     double* state, int64_t state_cap, void* ws, int64_t ws_bytes, int32_t* slot_busy,
+                     double* state, int64_t state_cap, void* ws, int64_t ws_bytes, int32_t* sched,
                      int nslots, ttgbf_diag* diag, ttgbf_step_rec* rec, void* stream) {
-  if (rcfg.steps < 0 || rcfg.kf < 1 || nslots < 1) return TTGBF_E_ARG;
-  auto f = LAMBDA(const Ctx& c0, int i, double* smem) {
-    // claim a free workspace slot for this CTA's lifetime
-    int slot = 0;
-    if (c0.leader()) {
-      slot = i % nslots;
-#if ENGINE_DEVICE
-      while (atomicCAS(&slot_busy[slot], 0, 1) != 0) slot = (slot + 1) % nslots;
-#else
-      while (slot_busy[slot] != 0) slot = (slot + 1) % nslots;
-      slot_busy[slot] = 1;
-#endif
-    }
-    slot = (int)bcast_i(c0, slot);
+  if (rcfg.steps < 0 || rcfg.kf < 1 || nslots < 1 || nfilt < 1) return TTGBF_E_ARG;
+  const int64_t total = (int64_t)nfilt * rcfg.steps;
+  auto f = LAMBDA(const Ctx& c, int slot, double* smem) {
     Arena ar = make_arena(ws, ws_bytes, slot);
-    ttgbf_diag* dg = diag + i;
-    Ctx c = c0;
-    c.prof = dg->prof;
-    if (c.leader()) {
-      for (int q = 0; q < 16; ++q) dg->prof[q] = 0;
-      for (int q = 0; q < 8; ++q) dg->cycles[q] = 0;
-    }
-    c.sync();
+    int32_t* cursor = sched;
+    int32_t* ndone = sched + 1;
+    int32_t* lock = sched + 2;
+    int32_t* done = sched + 2 + nfilt;
     const int b = model->b;
-    int st = stage_run(c, ar, *model, *prior, gcfg, xcfg, rcfg, io + i, kstep + i, Z + (int64_t)i * rcfg.kf * b,
-                       probes, nprobes, seeds, nseeds, state_hdr + i, state + (int64_t)i * state_cap, state_cap, dg,
-                       rec + (int64_t)i * rcfg.steps, make_stage_smem(smem));
-    if (c.leader()) { dg->status = st; dg->ws_peak = (int64_t)ar.peak; }
-    c.sync();
+    while (true) {
+      int fsel = -1;
+      if (c.leader()) {
+        while (true) {
 #if ENGINE_DEVICE
-    __threadfence();
-    if (c.leader()) atomicExch(&slot_busy[slot], 0);
+          if (*(volatile int32_t*)ndone >= total) break;
+          const int g = (int)((unsigned)atomicAdd(cursor, 1) % (unsigned)nfilt);
+          if (*(volatile int32_t*)(done + g) >= rcfg.steps) continue;
+          if (atomicCAS(&lock[g], 0, 1) != 0) continue;
+          __threadfence();   // acquire: drop stale L1 lines of this filter's state
+          if (*(volatile int32_t*)(done + g) >= rcfg.steps) { atomicExch(&lock[g], 0); continue; }
+          fsel = g;
+          break;
 #else
-    slot_busy[slot] = 0;
+          if (*ndone >= total) break;
+          const int g = (int)((unsigned)((*cursor)++) % (unsigned)nfilt);
+          if (done[g] >= rcfg.steps || lock[g]) continue;
+          lock[g] = 1;
+          fsel = g;
+          break;
 #endif
+        }
+      }
+      fsel = (int)bcast_i(c, fsel);
+      if (fsel < 0) break;
+      const int i = fsel;
+      ttgbf_diag* dg = diag + i;
+      Ctx cc = c;
+      cc.prof = dg->prof;
+      const int sidx = done[i];
+      int st = stage_run_step(cc, ar, *model, *prior, gcfg, xcfg, rcfg, io + i, kstep + i,
+                              Z + (int64_t)i * rcfg.kf * b, probes, nprobes, seeds, nseeds, state_hdr + i,
+                              state + (int64_t)i * state_cap, state_cap, dg, rec + (int64_t)i * rcfg.steps + sidx,
+                              make_stage_smem(smem));
+      if (c.leader()) {
+        dg->status = st;
+        if ((int64_t)ar.peak > dg->ws_peak) dg->ws_peak = (int64_t)ar.peak;
+      }
+      c.sync();
+      if (c.leader()) {
+#if ENGINE_DEVICE
+        __threadfence();
+        done[i] = sidx + 1;
+        __threadfence();
+        atomicAdd(ndone, 1);
+        atomicExch(&lock[i], 0);
+#else
+        done[i] = sidx + 1;
+        *ndone += 1;
+        lock[i] = 0;
+#endif
+      }
+      c.sync();
+    }
   };
-  return launch(nfilt, f, stream);
+  return launch(nslots < nfilt ? nslots : nfilt, f, stream);
 }
 
 // ---------------------------------------------------------------- TT primitives
@@ -233,12 +261,11 @@ int ttgbf_tt_interpolate(const ttgbf_tt* in_hdr, const double* in, int64_t in_ca
 
 int ttgbf_tt_eval_many(const ttgbf_tt* hdr, const double* data, int64_t cap, int count, const int32_t* idx, int64_t K,
                        double* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream) {
-  (void)ws;
-  (void)ws_bytes;
   auto f = LAMBDA(const Ctx& c, int i, double* smem) {
     const int d = hdr[i].d;
-    int st = body_eval_many(c, hdr + i, data + (int64_t)i * cap, idx + (int64_t)i * K * d, K, out + (int64_t)i * K,
-                            make_stage_smem(smem).sm);
+    Arena ar = make_arena(ws, ws_bytes, i);
+    int st = body_eval_many(c, ar, hdr + i, data + (int64_t)i * cap, idx + (int64_t)i * K * d, K,
+                            out + (int64_t)i * K, make_stage_smem(smem).sm);
     if (c.leader()) status[i] = st;
   };
   return launch(count, f, stream);

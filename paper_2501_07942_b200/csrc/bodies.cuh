@@ -84,14 +84,14 @@ HDN int body_interp(const Ctx& c, Arena& ar, const ttgbf_tt* ih, const double* i
   return tt_store(c, r, oh, out, ocap);
 }
 
-HDN int body_eval_many(const Ctx& c, const ttgbf_tt* h, const double* data, const int32_t* idx,
+HDN int body_eval_many(const Ctx& c, Arena& ar, const ttgbf_tt* h, const double* data, const int32_t* idx,
                               int64_t K, double* out, double* sm) {
   TT t = tt_view(h, const_cast<double*>(data));
   int maxr = 1;
   for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
   if (maxr > 512) return E_ARG;
-  tt_eval_idx(c, t, idx, K, out, sm);
-  return OK;
+  IndexSlice is{&t, idx, 0};
+  return tt_eval_bucketed(c, ar, t, K, is, out, sm);
 }
 
 
@@ -106,8 +106,7 @@ HDN int body_eval_points(const Ctx& c, Arena& ar, const ttgbf_tt* h, const doubl
   double st[MAXD];
   CK(materialize_axes(c, ar, t.d, axes, ax, geo, st));
   PointSlice<PtsFn> ps{&t, geo, PtsFn{pts, t.d}, 0, 0.0};
-  tt_chain_eval(c, t, K, ps, out, sm);
-  return OK;
+  return tt_eval_bucketed(c, ar, t, K, ps, out, sm);
 }
 
 HDN int body_moments(const Ctx& c, Arena& ar, const ttgbf_tt* h, const double* data, const ttgbf_axis* axes,

@@ -373,88 +373,100 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
 // calls with device geometry, restarting from the prior after a failure or
 // at the end of its trajectory (bench / Monte Carlo driver).
 // ---------------------------------------------------------------------------
+// one step of the persistent run for this filter; R receives the record
+HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_gauss& prior,
+                       const ttgbf_grid_cfg& gcfg, const ttgbf_cross_cfg& xcfg, const ttgbf_run_cfg& rc,
+                       ttgbf_filter_io* io, int32_t* kstep, const double* Z, const int32_t* probes, int nprobes,
+                       const int32_t* seeds, int nseeds, ttgbf_tt* hdr, double* state, int64_t cap,
+                       ttgbf_diag* dg, ttgbf_step_rec* R, StageSmem S) {
+  const int d = model.d, b = model.b;
+  const size_t mbase = ar.mark();
+  GeomOut* go;
+  ALLOC(go, GeomOut, 1, ar);
+  const size_t m0 = ar.mark();
+  if (!io->active) {
+    if (c.leader()) {
+      for (int k = 0; k < MAXD; ++k) io->cur[k] = rc.prior_grid[k];
+      *kstep = 0;
+      dg->clipped_mass = 0.0;
+    }
+    c.sync();
+    const int st = stage_prior(c, ar, model, prior, gcfg, xcfg, *io, probes, nprobes, hdr, state, cap, dg, S);
+    ar.release(m0);
+    if (st) {
+      if (c.leader()) { R->status = -1; R->k = -1; }
+      c.sync();
+      ar.release(mbase);
+      return OK;
+    }
+    if (c.leader()) io->active = 1;
+    c.sync();
+  }
+  const int kk = *kstep;
+  if (c.leader()) {
+    for (int i = 0; i < b; ++i) io->z[i] = Z[(int64_t)kk * b + i];
+    io->has_z = 1;
+    dg->clipped_mass = 0.0;
+    dg->outlier = 0;
+    R->k = kk;
+    for (int q = 0; q < 3; ++q) dg->cross[q].calls = 0;
+    for (int sl = 0; sl < 8; ++sl)
+      for (int k = 0; k <= TTGBF_MAXD; ++k) dg->ranks[sl][k] = 0;
+  }
+  c.sync();
+  int st = stage_measure(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S);
+  ar.release(m0);
+  if (!st) {
+    int gst = 0;
+    if (c.leader()) {
+      double dv = 1.0;
+      for (int k = 0; k < d; ++k)
+        dv *= (axis_at(io->cur[k], io->cur[k].n - 1) - axis_at(io->cur[k], 0)) / (double)(io->cur[k].n - 1);
+      if (!geom_moments(dg->raw_moments, d, dv, go)) {
+        gst = E_DEGENERATE;
+      } else if (!geom_redesign(go, d, model.F, model.Q, model.Finv, rc.n_per_axis, rc.sigma_mult, io->filt,
+                                io->pred)) {
+        gst = E_ARG;
+      } else {
+        for (int i = 0; i < d; ++i) { R->mean[i] = go->mean[i]; R->cov_diag[i] = go->cov[i * d + i]; }
+        R->spd_fixed = go->spd_fixed;
+      }
+    }
+    st = (int)bcast_i(c, gst);
+  }
+  if (!st) {
+    st = stage_time(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S);
+    ar.release(m0);
+  }
+  if (c.leader()) {
+    R->status = st;
+    R->outlier = dg->outlier;
+    R->mass_before_norm = dg->mass_before_norm;
+    R->clipped_mass = dg->clipped_mass;
+    for (int q = 0; q < 3; ++q) R->calls[q] = dg->cross[q].calls;
+    for (int sl = 0; sl < 8; ++sl)
+      for (int k = 0; k <= TTGBF_MAXD; ++k) R->ranks[sl][k] = dg->ranks[sl][k];
+    if (st) {
+      io->active = 0;
+    } else {
+      for (int k = 0; k < MAXD; ++k) io->cur[k] = io->pred[k];
+      *kstep = kk + 1;
+      if (kk + 1 >= rc.kf) io->active = 0;
+    }
+  }
+  c.sync();
+  ar.release(mbase);
+  return OK;
+}
+
 HDN int stage_run(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_gauss& prior,
                   const ttgbf_grid_cfg& gcfg, const ttgbf_cross_cfg& xcfg, const ttgbf_run_cfg& rc,
                   ttgbf_filter_io* io, int32_t* kstep, const double* Z, const int32_t* probes, int nprobes,
                   const int32_t* seeds, int nseeds, ttgbf_tt* hdr, double* state, int64_t cap, ttgbf_diag* dg,
                   ttgbf_step_rec* rec, StageSmem S) {
-  const int d = model.d, b = model.b;
-  GeomOut* go;
-  ALLOC(go, GeomOut, 1, ar);
-  const size_t m0 = ar.mark();
-  for (int s = 0; s < rc.steps; ++s) {
-    ttgbf_step_rec* R = rec + s;
-    if (!io->active) {
-      if (c.leader()) {
-        for (int k = 0; k < MAXD; ++k) io->cur[k] = rc.prior_grid[k];
-        *kstep = 0;
-        dg->clipped_mass = 0.0;
-      }
-      c.sync();
-      const int st = stage_prior(c, ar, model, prior, gcfg, xcfg, *io, probes, nprobes, hdr, state, cap, dg, S);
-      ar.release(m0);
-      if (st) {
-        if (c.leader()) { R->status = -1; R->k = -1; }
-        c.sync();
-        continue;
-      }
-      if (c.leader()) io->active = 1;
-      c.sync();
-    }
-    const int kk = *kstep;
-    if (c.leader()) {
-      for (int i = 0; i < b; ++i) io->z[i] = Z[(int64_t)kk * b + i];
-      io->has_z = 1;
-      dg->clipped_mass = 0.0;
-      dg->outlier = 0;
-      R->k = kk;
-      for (int q = 0; q < 3; ++q) dg->cross[q].calls = 0;
-      for (int sl = 0; sl < 8; ++sl)
-        for (int k = 0; k <= TTGBF_MAXD; ++k) dg->ranks[sl][k] = 0;
-    }
-    c.sync();
-    int st = stage_measure(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S);
-    ar.release(m0);
-    if (!st) {
-      int gst = 0;
-      if (c.leader()) {
-        double dv = 1.0;
-        for (int k = 0; k < d; ++k)
-          dv *= (axis_at(io->cur[k], io->cur[k].n - 1) - axis_at(io->cur[k], 0)) / (double)(io->cur[k].n - 1);
-        if (!geom_moments(dg->raw_moments, d, dv, go)) {
-          gst = E_DEGENERATE;
-        } else if (!geom_redesign(go, d, model.F, model.Q, model.Finv, rc.n_per_axis, rc.sigma_mult, io->filt,
-                                  io->pred)) {
-          gst = E_ARG;
-        } else {
-          for (int i = 0; i < d; ++i) { R->mean[i] = go->mean[i]; R->cov_diag[i] = go->cov[i * d + i]; }
-          R->spd_fixed = go->spd_fixed;
-        }
-      }
-      st = (int)bcast_i(c, gst);
-    }
-    if (!st) {
-      st = stage_time(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S);
-      ar.release(m0);
-    }
-    if (c.leader()) {
-      R->status = st;
-      R->outlier = dg->outlier;
-      R->mass_before_norm = dg->mass_before_norm;
-      R->clipped_mass = dg->clipped_mass;
-      for (int q = 0; q < 3; ++q) R->calls[q] = dg->cross[q].calls;
-      for (int sl = 0; sl < 8; ++sl)
-        for (int k = 0; k <= TTGBF_MAXD; ++k) R->ranks[sl][k] = dg->ranks[sl][k];
-      if (st) {
-        io->active = 0;
-      } else {
-        for (int k = 0; k < MAXD; ++k) io->cur[k] = io->pred[k];
-        *kstep = kk + 1;
-        if (kk + 1 >= rc.kf) io->active = 0;
-      }
-    }
-    c.sync();
-  }
+  for (int s = 0; s < rc.steps; ++s)
+    CK(stage_run_step(c, ar, model, prior, gcfg, xcfg, rc, io, kstep, Z, probes, nprobes, seeds, nseeds, hdr, state,
+                      cap, dg, rec + s, S));
   return OK;
 }
 

@@ -478,53 +478,43 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
       c.sync();
 #if ENGINE_DEVICE
       {
+        // DMMA tiles: 8 points x 8 output columns, k-steps of 4 over rl.
+        // Fragments (PTX m8n8k4 .f64): A(row=lane/4, col=lane%4),
+        // B(row=lane%4, col=lane/4), C(row=lane/4, cols 2*(lane%4)+{0,1}).
         const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
-        for (int q0 = beg + 2 * warp; q0 < end; q0 += 2 * nwarps) {
-          const bool has1 = q0 + 1 < end;
-          const int p0 = perm[q0], p1 = has1 ? perm[q0 + 1] : p0;
-          const double wl0 = wlv[p0], wh0 = whv[p0], wl1 = wlv[p1], wh1 = whv[p1];
-          double v0[2], v1[2], a0[2], a1[2];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int a = h * 32 + lane;
-            v0[h] = a < rl ? Vin[(int64_t)p0 * maxr + a] : 0.0;
-            v1[h] = a < rl ? Vin[(int64_t)p1 * maxr + a] : 0.0;
-            a0[h] = 0.0;
-            a1[h] = 0.0;
-          }
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (h * 32 < rl) {
-              const int amax = imin(32, rl - h * 32);
-#pragma unroll 4
-              for (int l = 0; l < amax; ++l) {
-                const double va0 = __shfl_sync(0xffffffffu, v0[h], l);
-                const double va1 = __shfl_sync(0xffffffffu, v1[h], l);
-                const int a = h * 32 + l;
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                  const int bb = q * 32 + lane;
-                  if (bb < rr) {
-                    const double xa = A[a * rr + bb];
-                    double x0 = xa, x1 = xa;
-                    if (Slice::kBlend) {
-                      const double xb = B[a * rr + bb];
-                      x0 = xa * wl0 + xb * wh0;
-                      x1 = xa * wl1 + xb * wh1;
-                    }
-                    a0[q] = fma(va0, x0, a0[q]);
-                    a1[q] = fma(va1, x1, a1[q]);
-                  }
-                }
+        const int ar = lane >> 2, ac = lane & 3;
+        for (int q0 = beg + 8 * warp; q0 < end; q0 += 8 * nwarps) {
+          const int qa = q0 + ar;
+          const bool rv = qa < end;
+          const int pa = rv ? perm[qa] : perm[q0];
+          const double* vrow = Vin + (int64_t)pa * maxr;
+          const double wl = wlv[pa], wh = whv[pa];
+          for (int n0 = 0; n0 < rr; n0 += 8) {
+            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+            const int bcol = n0 + ar;
+            for (int k0 = 0; k0 < rl; k0 += 4) {
+              const int ka = k0 + ac;
+              const double af = (rv && ka < rl) ? vrow[ka] : 0.0;
+              const bool bv = ka < rl && bcol < rr;
+              const double bf = bv ? A[ka * rr + bcol] : 0.0;
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                           : "+d"(c0), "+d"(c1) : "d"(af), "d"(bf));
+              if (Slice::kBlend) {
+                const double bf2 = bv ? B[ka * rr + bcol] : 0.0;
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(e0), "+d"(e1) : "d"(af), "d"(bf2));
               }
             }
-          }
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int bb = q * 32 + lane;
-            if (bb < rr) {
-              Vout[(int64_t)p0 * maxr + bb] = a0[q];
-              if (has1) Vout[(int64_t)p1 * maxr + bb] = a1[q];
+            if (rv) {
+              const int oc = n0 + 2 * ac;
+              double* orow = Vout + (int64_t)pa * maxr;
+              if (Slice::kBlend) {
+                if (oc < rr) orow[oc] = c0 * wl + e0 * wh;
+                if (oc + 1 < rr) orow[oc + 1] = c1 * wl + e1 * wh;
+              } else {
+                if (oc < rr) orow[oc] = c0;
+                if (oc + 1 < rr) orow[oc + 1] = c1;
+              }
             }
           }
         }
@@ -534,13 +524,12 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
         const int p = perm[q0];
         const double wl = wlv[p], wh = whv[p];
         for (int bb = 0; bb < rr; ++bb) {
-          double acc = 0.0;
+          double acc = 0.0, acc2 = 0.0;
           for (int a = 0; a < rl; ++a) {
-            double x = A[a * rr + bb];
-            if (Slice::kBlend) x = x * wl + B[a * rr + bb] * wh;
-            acc = fma(Vin[(int64_t)p * maxr + a], x, acc);
+            acc = fma(Vin[(int64_t)p * maxr + a], A[a * rr + bb], acc);
+            if (Slice::kBlend) acc2 = fma(Vin[(int64_t)p * maxr + a], B[a * rr + bb], acc2);
           }
-          Vout[(int64_t)p * maxr + bb] = acc;
+          Vout[(int64_t)p * maxr + bb] = Slice::kBlend ? acc * wl + acc2 * wh : acc;
         }
       }
 #endif

@@ -242,7 +242,8 @@ def tt_eval_many(tt: TensorTrain, idx) -> np.ndarray:
     out = be.empty(8 * K)
     st = be.empty(4)
     hh = _hdr_dev(tt)
-    rc = be.lib.ttgbf_tt_eval_many(hh.ptr, tt.data.data_ptr(), tt.size, 1, di.ptr, K, out.ptr, None, 0,
+    ws = _ws(WS_BYTES)
+    rc = be.lib.ttgbf_tt_eval_many(hh.ptr, tt.data.data_ptr(), tt.size, 1, di.ptr, K, out.ptr, ws.ptr, WS_BYTES,
                                    st.ptr, be.stream_ptr)
     be.check(rc, "tt_eval_many")
     _status(be.download(st, np.int32, 1)[0], "tt_eval_many")

@@ -126,3 +126,23 @@ def compare_scenario_run(golden, name, backend):
     rows.append({"step": "final", "dens": rel(T.to_full(got), T.to_full(ref)),
                  "ranks": (T.ranks_of(got), T.ranks_of(ref))})
     return rows
+
+
+def check_large_eval(golden, case):
+    """tt_eval_many / tt_eval_at_points on batches large enough for the
+    bucketed (SMEM-staged / DMMA) evaluation path."""
+    from paper_2501_07942_b200 import tensor_train as G
+    from paper_2501_07942_b200.grids import Grid
+    from paper_2501_07942_b200 import geometry as geo
+    z = golden("primitives")
+    cores = load_tt(z, f"{case}/a")
+    a = G.TensorTrain.from_cores(cores)
+    shape = a.shape
+    rng = np.random.default_rng(5)
+    idx = np.stack([rng.integers(0, n, 5000) for n in shape], axis=1)
+    assert rel(G.tt_eval_many(a, idx), T.at_indices(cores, idx)) <= 1e-13
+    cuts = np.cumsum(shape)[:-1]
+    old = np.split(z[f"{case}/old_axes"], cuts)
+    og = Grid(geo.grid_from_bounds([o[0] for o in old], [o[-1] for o in old], list(shape)))
+    pts = np.column_stack([rng.uniform(ax[0] - 0.2, ax[-1] + 0.2, 5000) for ax in og.axes])
+    assert rel(G.tt_eval_at_points(a, og, pts), T.at_points(cores, og.axes, pts)) <= 1e-13

@@ -34,3 +34,10 @@ def test_persistent_run_hostsim(golden, backend, name):
                 assert r[key] <= tol, r
         if "ranks" in r:
             assert r["ranks"][0] == r["ranks"][1], r
+
+
+@pytest.mark.parametrize("case", ["s3", "s4", "s6"])
+def test_large_eval_hostsim(golden, backend, case):
+    from scenario_util import check_large_eval, use_backend
+    use_backend(backend)
+    check_large_eval(golden, case)

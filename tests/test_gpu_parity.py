@@ -43,3 +43,10 @@ def test_round_rank_deficient_gpu(golden, cuda):
     ref = load_tt(z, "sq/round")
     assert got.ranks == T.ranks_of(ref)
     assert rel(T.to_full(got.numpy_cores()), T.to_full(ref)) <= 1e-12
+
+
+@pytest.mark.parametrize("case", ["s3", "s4", "s6"])
+def test_large_eval_gpu(golden, cuda, case):
+    from scenario_util import check_large_eval, use_backend
+    use_backend(cuda)
+    check_large_eval(golden, case)
