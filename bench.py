@@ -35,7 +35,8 @@ sys.path.insert(0, ROOT)
 from paper_2501_07942_b200.configs import BASELINE_CONFIGS, simulate  # noqa: E402
 
 PROF_NAMES = ["miss_sort", "evaluator", "cache_eval", "core_lstsq", "hunt", "accept", "cache_check", "tt_round",
-              "svd", "qr", "rng_choice", "snapshot", "chain_eval", "inject", "fft_conv", "neg_mass"]
+              "svd", "qr", "rng_choice", "snapshot", "chain_eval", "inject", "fft_conv", "neg_mass",
+              "qr_panel", "qr_update", "round_rmul", "round_applyq", "fft_product", "svd_rrqr"]
 METRIC = "TT-GBF filter steps/s (d=6, N_pa=64, rank<=20)"
 WORKLOAD = "C5: d=6 CV, N_pa=64 (run as 65), rank cap 20, round tol 1e-8, cross tol 1e-2/max_rank 40, sigma 6"
 
@@ -49,9 +50,12 @@ def parse():
     p.add_argument("--slots", type=int, default=296)   # resident CTAs: 2 per SM x 148
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C5")
-    p.add_argument("--ws-mb", type=int, default=512)
+    p.add_argument("--ws-mb", type=int, default=384)      # per resident CTA slot
+    p.add_argument("--big-slots", type=int, default=40)   # overflow workspaces for oversized FFT products
+    p.add_argument("--big-mb", type=int, default=1280)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-s", type=float, default=20.0)
+    p.add_argument("--dump", default=None, help="save the timed run's step records (npz) for analysis")
     return p.parse_args()
 
 
@@ -208,8 +212,9 @@ def run_ours(args):
     B = args.batch
     bcfg = BankConfig(n_per_axis=g["n_per_axis"], sigma_mult=g["sigma_mult"], round_tol=g["round_tol"],
                       round_max_rank=g["round_max_rank"], tol=x["tol"], max_rank=x["max_rank"],
-                      rng_seed=x["rng_seed"], ws_bytes=args.ws_mb << 20, state_doubles=1 << 19,
-                      cache_cap=1 << 20, ws_slots=args.slots)
+                      rng_seed=x["rng_seed"], ws_bytes=args.ws_mb << 20, state_doubles=1 << 17,
+                      cache_cap=1 << 20, ws_slots=args.slots, big_slots=args.big_slots,
+                      big_bytes=args.big_mb << 20)
     d = cfg["spec"]["F"].shape[0]
     b = np.atleast_2d(cfg["spec"]["R"]).shape[0]
     n = g["n_per_axis"]
@@ -220,7 +225,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     peak_fp64 = rl.measure_fp64_peak(torch, dev)
     bank = FilterBank(cfg["spec"], bcfg, B)
-    stats = {"flops": 0.0, "cycles": np.zeros(8), "prof": np.zeros(16), "ranks": None}
+    stats = {"flops": 0.0, "cycles": np.zeros(8), "prof": np.zeros(32), "ranks": None}
 
     # warm-up: W filter steps per filter (one persistent launch)
     if args.warmup:
@@ -238,6 +243,8 @@ def run_ours(args):
     if world > 1:
         torch.distributed.barrier()
     dg = bank._diag()
+    if args.dump:
+        np.savez_compressed(args.dump, recs=recs, cycles=dg["cycles"], prof=dg["prof"])
     ok = recs["status"] == 0
     stats["completed"] = int(ok.sum())
     stats["failed"] = int((recs["status"] > 0).sum())
@@ -249,9 +256,15 @@ def run_ours(args):
         step_fl.append(fl)
     step_fl = np.array(step_fl) if step_fl else np.zeros(1)
     stats["step_gflop_pcts"] = [round(float(np.percentile(step_fl, q)) / 1e9, 3) for q in (50, 90, 99, 100)]
+    cyc = recs["cycles"][recs["status"] >= 0].astype(float) / 1.965e9
+    stats["step_ms_pcts"] = [round(1e3 * float(np.percentile(cyc, q)), 2) for q in (50, 90, 99, 100)] if cyc.size else None
+    stats["step_sm_s_total"] = float(recs["cycles"].astype(float).sum() / 1.965e9)
     stats["cycles"] = dg["cycles"].sum(axis=0).astype(float)
     stats["prof"] = dg["prof"].sum(axis=0).astype(float)
     stats["ws_peak"] = int(dg["ws_peak"].max())
+    stats["big_used"] = int(dg["big_used"].sum())
+    stats["big_peak"] = int(dg["big_peak"].max())
+    stats["big_wait_s"] = float(dg["big_wait"].sum() / 1.965e9)
     att = recs["status"] >= 0
     stats["calls"] = {nm: float(recs["calls"][:, :, q][att].mean()) if att.any() else 0.0
                       for q, nm in enumerate(["likelihood", "kernel", "realign"])}
@@ -310,11 +323,22 @@ def run_ours(args):
         "kernel_time_s": {k: sum(v) for k, v in per_kernel.items()},
         "device_busy_frac": kern_total / dev_s if dev_s > 0 else None,
         "stage_cycles_share": (stats["cycles"] / max(stats["cycles"].sum(), 1)).round(4).tolist(),
-        "engine_prof_share": dict(zip(PROF_NAMES, (stats["prof"] / max(stats["cycles"].sum(), 1)).round(4).tolist())),
+        "engine_prof_share": dict(zip(PROF_NAMES, (stats["prof"][:22] / max(stats["cycles"].sum(), 1)).round(4).tolist())),
+        "svd_rrqr_mean_rank": float(stats["prof"][22] / max(stats["prof"][23], 1)),
+        "svd_detail": {"max_rank": int(dg["prof"][:, 24].max()),
+                       "jacobi": round(float(stats["prof"][25] / max(stats["cycles"].sum(), 1)), 4),
+                       "u_apply": round(float(stats["prof"][26] / max(stats["cycles"].sum(), 1)), 4),
+                       "bt_qr_v": round(float(stats["prof"][27] / max(stats["cycles"].sum(), 1)), 4),
+                       "calls_rank_gt64": int(stats["prof"][28]),
+                       "share_rank_gt64": round(float(stats["prof"][29] / max(stats["cycles"].sum(), 1)), 4)},
         "completed_frac": stats["completed"] / max(1, B * args.steps),
         "ws_peak_mb": stats["ws_peak"] / 2 ** 20,
+        "overflow_ws": {"slots": args.big_slots, "mb": args.big_mb, "steps_used": stats["big_used"],
+                        "peak_mb": stats["big_peak"] / 2 ** 20, "cta_seconds_waiting": stats["big_wait_s"]},
         "mean_cross_calls": stats["calls"],
         "step_gflop_p50_p90_p99_max": stats["step_gflop_pcts"],
+        "step_ms_p50_p90_p99_max": stats["step_ms_pcts"],
+        "cta_seconds_in_steps": stats["step_sm_s_total"],
         "stage_sm_seconds_per_attempted_step": stats["stage_s_per_step"],
         "example_ranks": stats["ranks"],
         "rmse": rmse,

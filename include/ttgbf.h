@@ -121,8 +121,15 @@ typedef struct {
   /* engine profile (SM cycles, CTA leader, overlapping categories):
    * 0 miss sort, 1 evaluator, 2 cache lookup/insert, 3 core lstsq, 4 hunt,
    * 5 accept, 6 cache check, 7 tt_round, 8 svd, 9 qr, 10 rng choice,
-   * 11 snapshot, 12 chain eval, 13 inject, 14 fft conv body, 15 negative mass */
-  int64_t prof[16];
+   * 11 snapshot, 12 chain eval, 13 inject, 14 fft conv (incl. round),
+   * 15 negative mass, 16 qr panel, 17 qr trailing update, 18 round R-multiply,
+   * 19 round apply_q, 20 fft spectra+product, 21 svd rrqr, 22 rrqr rank sum (count, not cycles), 23 svd_rrqr calls,
+   * 24 max rrqr rank (count), 25 svd jacobi, 26 svd U from reflectors, 27 svd Bt QR + V,
+   * 28 svd calls with rank > 64 (count), 29 their cycles, 30-31 spare */
+  int64_t prof[32];
+  int64_t big_used;       /* steps that borrowed an overflow workspace */
+  int64_t big_peak;       /* peak bytes used in an overflow workspace */
+  int64_t big_wait;       /* SM cycles spent waiting for a free overflow workspace */
 } ttgbf_diag;
 
 /* Model constants (StateSpaceModel, models.py:85-153).  Matrices row-major
@@ -175,6 +182,15 @@ typedef struct {
   int32_t pad;
   double sigma_mult;
   ttgbf_axis prior_grid[TTGBF_MAXD];
+  /* overflow workspaces: a step whose FFT product (kernel rank x filter rank
+   * per bond) does not fit in its slot borrows one of nbig buffers of
+   * big_bytes for the convolution + rounding (spin-acquired, big_locks
+   * zero-initialised), then copies the rounded TT back.  nbig = 0: none. */
+  int32_t nbig;
+  int32_t pad2;
+  int64_t big_bytes;
+  void* big_ws;
+  int32_t* big_locks;
 } ttgbf_run_cfg;
 
 /* one record per filter per attempted step */
@@ -189,6 +205,7 @@ typedef struct {
   double clipped_mass;
   int64_t calls[3];
   int32_t ranks[8][TTGBF_MAXD + 1];
+  int64_t cycles;         /* SM clock cycles the step took on its CTA (0 in host emulation) */
 } ttgbf_step_rec;
 
 /* io[f].active is the filter's alive flag and io[f].cur its grid (in/out);

@@ -33,7 +33,8 @@ CROSS_INFO = np.dtype([("achieved", "f8"), ("calls", "i8"), ("sweeps", "i4"), ("
 DIAG = np.dtype([("status", "i4"), ("outlier", "i4"), ("mass_before_norm", "f8"),
                  ("clipped_mass", "f8"), ("cross", CROSS_INFO, 3), ("raw_moments", "f8", NMOM),
                  ("ws_peak", "i8"), ("ranks", "i4", (8, MAXD + 1)), ("cycles", "i8", 8),
-                 ("prof", "i8", 16)], align=True)
+                 ("prof", "i8", 32), ("big_used", "i8"), ("big_peak", "i8"),
+                 ("big_wait", "i8")], align=True)
 MODEL = np.dtype([("d", "i4"), ("b", "i4"), ("hkind", "i4"), ("nang", "i4"), ("ang", "i4", MAXB),
                   ("F", "f8", MAXD * MAXD), ("Finv", "f8", MAXD * MAXD), ("Lq", "f8", MAXD * MAXD),
                   ("logn_q", "f8"), ("Lr", "f8", MAXB * MAXB), ("logn_r", "f8"),
@@ -42,7 +43,7 @@ GAUSS = np.dtype([("mean", "f8", MAXD), ("L", "f8", MAXD * MAXD), ("logn", "f8")
 RUN_CFG_FIELDS = None
 STEP_REC = np.dtype([("status", "i4"), ("k", "i4"), ("spd_fixed", "i4"), ("outlier", "i4"), ("mean", "f8", MAXD),
                      ("cov_diag", "f8", MAXD), ("mass_before_norm", "f8"), ("clipped_mass", "f8"),
-                     ("calls", "i8", 3), ("ranks", "i4", (8, MAXD + 1))], align=True)
+                     ("calls", "i8", 3), ("ranks", "i4", (8, MAXD + 1)), ("cycles", "i8")], align=True)
 FILTER_IO = np.dtype([("cur", AXIS, MAXD), ("filt", AXIS, MAXD), ("pred", AXIS, MAXD),
                       ("z", "f8", MAXB), ("has_z", "i4"), ("active", "i4")], align=True)
 
@@ -59,7 +60,9 @@ class Axis(ctypes.Structure):
 
 class RunCfg(ctypes.Structure):
     _fields_ = [("n_per_axis", ctypes.c_int32), ("kf", ctypes.c_int32), ("steps", ctypes.c_int32),
-                ("pad", ctypes.c_int32), ("sigma_mult", ctypes.c_double), ("prior_grid", Axis * MAXD)]
+                ("pad", ctypes.c_int32), ("sigma_mult", ctypes.c_double), ("prior_grid", Axis * MAXD),
+                ("nbig", ctypes.c_int32), ("pad2", ctypes.c_int32), ("big_bytes", ctypes.c_int64),
+                ("big_ws", ctypes.c_void_p), ("big_locks", ctypes.c_void_p)]
 
 
 class CrossCfg(ctypes.Structure):

@@ -52,6 +52,8 @@ class BankConfig:
     state_doubles: int = 1 << 20
     cache_cap: int = 1 << 20
     ws_slots: int = 0          # persistent run: workspace slots (0 = one per filter)
+    big_slots: int = 0         # persistent run: overflow workspaces for oversized FFT products
+    big_bytes: int = 3 << 29
 
     def grid_cfg(self):
         return _abi.GridCfg(self.round_tol, int(self.round_max_rank or 0),
@@ -161,6 +163,9 @@ class FilterBank:
         self.nslots = min(n, cfg.ws_slots) if cfg.ws_slots > 0 else n
         self.ws = backend.empty(self.nslots * cfg.ws_bytes)
         self.sched = backend.empty(4 * (2 + 2 * n))
+        self.nbig = int(cfg.big_slots)
+        self.big_ws = backend.empty(self.nbig * cfg.big_bytes) if self.nbig else None
+        self.big_locks = backend.empty(4 * max(1, self.nbig))
         self.diag_dev = backend.empty(n * _abi.DIAG.itemsize)
         self.grids: list[geo.Axes | None] = [None] * n
         self.alive = np.zeros(n, dtype=bool)
@@ -329,6 +334,11 @@ class FilterBank:
             rc.prior_grid[k].off = int(dev["off"][k])
             rc.prior_grid[k].n = int(dev["n"][k])
         self.be.zero(self.sched)
+        self.be.zero(self.big_locks)
+        rc.nbig = self.nbig
+        rc.big_bytes = int(self.cfg.big_bytes)
+        rc.big_ws = self.big_ws.ptr if self.big_ws is not None else None
+        rc.big_locks = self.big_locks.ptr
         self.be.zero(self.diag_dev)
         zb = self.be.upload(Z)
         self.bytes_h2d += Z.nbytes

@@ -103,7 +103,7 @@ int ttgbf_filter_measure(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cr
     c.prof = dg->prof;
     if (c.leader()) {
       dg->clipped_mass = 0.0; dg->outlier = 0; dg->mass_before_norm = NAN;
-      for (int q = 0; q < 16; ++q) dg->prof[q] = 0;
+      for (int q = 0; q < 32; ++q) dg->prof[q] = 0;
       for (int q = 0; q < 8; ++q) dg->cycles[q] = 0;
     }
     c.sync();

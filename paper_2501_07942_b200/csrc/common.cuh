@@ -228,6 +228,16 @@ struct Arena {
   HD void release(size_t m) { off = m; }
 };
 
+// arena over slot `item` of a slab of equal workspaces
+HD Arena make_ws_arena(void* ws, int64_t ws_bytes, int item) {
+  Arena a;
+  a.base = reinterpret_cast<char*>(ws) + (int64_t)item * ws_bytes;
+  a.cap = (size_t)ws_bytes;
+  a.off = 0;
+  a.peak = 0;
+  return a;
+}
+
 #define ALLOC(ptr, T, n, ar) do { (ptr) = (ar).template alloc<T>((size_t)(n)); if (!(ptr)) return ::tg::E_WORKSPACE; } while (0)
 
 // ---------------------------------------------------------------------------

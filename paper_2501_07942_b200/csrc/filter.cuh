@@ -301,10 +301,53 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
 // ---------------------------------------------------------------------------
 // time update of tt_fft_pmf_step (filters.py:958-985)
 // ---------------------------------------------------------------------------
+// FFT convolution + rounding inside a borrowed overflow workspace; the
+// rounded TT (small) is copied back into the slot arena at `mark`.
+HDN int conv_in_overflow(const Ctx& c, Arena& ar, size_t mark, const TT& ker, const TT& shifted,
+                         const ttgbf_grid_cfg& gcfg, const ttgbf_run_cfg& pool, ttgbf_diag* dg, TT& conv,
+                         double* sm) {
+  int bi = -1;
+  if (c.leader()) {
+#if ENGINE_DEVICE
+    const int64_t tw = clk();
+    while (bi < 0) {
+      for (int i = 0; i < pool.nbig && bi < 0; ++i)
+        if (atomicCAS(&pool.big_locks[i], 0, 1) == 0) bi = i;
+      if (bi < 0) __nanosleep(4000);
+    }
+    dg->big_wait += clk() - tw;
+#else
+    bi = 0;
+#endif
+  }
+  bi = (int)bcast_i(c, bi);
+  Arena big = make_ws_arena(pool.big_ws, pool.big_bytes, bi);
+  TT big_conv;
+  int st = tt_fft_conv(c, big, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, big_conv, sm);
+  if (!st) {
+    ar.release(mark);
+    st = tt_alloc(ar, conv, big_conv.d, big_conv.n, big_conv.r);
+    if (!st) {
+      for (int k = 0; k < conv.d; ++k) par_copy(c, conv.c[k], big_conv.c[k], conv.size(k));
+    }
+  }
+  c.sync();
+  if (c.leader()) {
+    dg->big_used += 1;
+    if ((int64_t)big.peak > dg->big_peak) dg->big_peak = (int64_t)big.peak;
+#if ENGINE_DEVICE
+    __threadfence();
+    atomicExch(&pool.big_locks[bi], 0);
+#endif
+  }
+  c.sync();
+  return st;
+}
+
 HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_grid_cfg& gcfg,
                           const ttgbf_cross_cfg& xcfg, const ttgbf_filter_io& io, const int32_t* probes,
                           int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* hdr, double* state,
-                          int64_t cap, ttgbf_diag* dg, StageSmem S) {
+                          int64_t cap, ttgbf_diag* dg, StageSmem S, const ttgbf_run_cfg* pool = nullptr) {
   const int d = model.d;
   double *ac[MAXD], *af[MAXD], *apd[MAXD];
   AxisGeom gc[MAXD], gf[MAXD], gp[MAXD];
@@ -339,8 +382,17 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   CK(tt_compact(c, ar, m1, ker));
   // FFT convolution + rounding
   TT conv;
-  CK(tt_fft_conv(c, ar, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, conv, S.sm));
-  CK(tt_compact(c, ar, m0, conv));
+  int64_t pbytes = 0;
+  for (int k = 0; k < d; ++k)
+    pbytes += (int64_t)ker.r[k] * shifted.r[k] * ker.n[k] * ker.r[k + 1] * shifted.r[k + 1] * 8;
+  const int64_t need = pbytes + pbytes / 16 + ((int64_t)64 << 20);   // + rounding temporaries
+  if (pool && pool->nbig > 0 && (int64_t)(ar.cap - ar.off) < need) {
+    if (need > pool->big_bytes) return E_WORKSPACE;
+    CK(conv_in_overflow(c, ar, m0, ker, shifted, gcfg, *pool, dg, conv, S.sm));
+  } else {
+    CK(tt_fft_conv(c, ar, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, conv, S.sm));
+    CK(tt_compact(c, ar, m0, conv));
+  }
   if (c.leader()) { log_ranks(dg, 5, conv); dg->cycles[5] += clk() - t0; }
   t0 = clk();
   int maxr = 1;
@@ -380,6 +432,7 @@ HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
                        const int32_t* seeds, int nseeds, ttgbf_tt* hdr, double* state, int64_t cap,
                        ttgbf_diag* dg, ttgbf_step_rec* R, StageSmem S) {
   const int d = model.d, b = model.b;
+  const int64_t t_start = clk();
   const size_t mbase = ar.mark();
   GeomOut* go;
   ALLOC(go, GeomOut, 1, ar);
@@ -394,7 +447,7 @@ HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
     const int st = stage_prior(c, ar, model, prior, gcfg, xcfg, *io, probes, nprobes, hdr, state, cap, dg, S);
     ar.release(m0);
     if (st) {
-      if (c.leader()) { R->status = -1; R->k = -1; }
+      if (c.leader()) { R->status = -1; R->k = -1; R->cycles = clk() - t_start; }
       c.sync();
       ar.release(mbase);
       return OK;
@@ -435,7 +488,7 @@ HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
     st = (int)bcast_i(c, gst);
   }
   if (!st) {
-    st = stage_time(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S);
+    st = stage_time(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S, &rc);
     ar.release(m0);
   }
   if (c.leader()) {
@@ -446,6 +499,7 @@ HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
     for (int q = 0; q < 3; ++q) R->calls[q] = dg->cross[q].calls;
     for (int sl = 0; sl < 8; ++sl)
       for (int k = 0; k <= TTGBF_MAXD; ++k) R->ranks[sl][k] = dg->ranks[sl][k];
+    R->cycles = clk() - t_start;
     if (st) {
       io->active = 0;
     } else {

@@ -101,6 +101,316 @@ HDN void gemm_t(const Ctx& c, int M, int N, int K, double alpha, Mat A, Mat B, d
 #endif
 }
 
+// DMMA tiled GEMM (256 threads): C = alpha*A*B + beta*C on FP64 tensor-core
+// tiles (mma.sync.m8n8k4.f64).  CTA tile 64 x TN x 16, warps 2 (m) x 4 (n),
+// warp tile 32 x TN/4.  SMEM double-buffered with register prefetch of the
+// next K-tile; each operand is staged in the layout that keeps both its
+// global loads (unit-stride dimension fastest) and the fragment reads
+// bank-conflict free:  K-major [16][68] when the operand's unit stride runs
+// along its M/N index, M/N-major [64][20] when it runs along K.
+// ktri: B(p, j) == 0 for p < j (B = R^T of an upper-triangular R), so column
+// tile j0 starts its K loop at j0.  SMEM: 2 * 2 * 1280 doubles.
+template <int TN>
+HDN void gemm_dm(const Ctx& c, int M, int N, int K, double alpha, Mat A, Mat B, double beta, double* C, int64_t crs,
+                 int64_t ccs, double* sm, bool ktri = false) {
+#if ENGINE_DEVICE
+  if (c.nt != 256) {
+    gemm_t<64>(c, M, N, K, alpha, A, B, beta, C, crs, ccs, sm);
+    return;
+  }
+  constexpr int TM = 64, TK = 16, LK = 68, LM = 20, OPS = 1280;
+  constexpr int WN = TN / 4, NT = WN / 8;        // warp tile columns, 8-wide n tiles per warp
+  constexpr int AL = TM * TK / 256, BL = TN * TK / 256;   // elements each thread loads per K-tile
+  const int warp = c.tid >> 5, lane = c.tid & 31;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int ar = lane >> 2, ac = lane & 3;
+  const bool a_kmaj = A.rs == 1;   // unit stride along i -> K-major staging
+  const bool b_kmaj = B.cs == 1;   // unit stride along j -> K-major staging
+  double ra[AL], rb[BL];
+  for (int i0 = 0; i0 < M; i0 += TM) {
+    for (int j0 = 0; j0 < N; j0 += TN) {
+      const int kbeg = ktri ? (j0 / TK) * TK : 0;
+      if (kbeg >= K) {
+        // whole K range is zero: C = beta*C
+        for (int e = c.tid; e < TM * TN; e += 256) {
+          const int gi = i0 + e / TN, gj = j0 + e % TN;
+          if (gi < M && gj < N) {
+            double* cp = C + gi * crs + gj * ccs;
+            *cp = (beta == 0.0) ? 0.0 : beta * (*cp);
+          }
+        }
+        continue;
+      }
+      double acc[4][NT][2];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < NT; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+      // global -> registers for K-tile p0
+      auto load = [&](int p0) {
+#pragma unroll
+        for (int q = 0; q < AL; ++q) {
+          const int e = c.tid + 256 * q;
+          int pp, ii;
+          if (a_kmaj) { ii = e % TM; pp = e / TM; } else { pp = e % TK; ii = e / TK; }
+          const int gi = i0 + ii, gp = p0 + pp;
+          ra[q] = (gi < M && gp < K) ? A.at(gi, gp) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < BL; ++q) {
+          const int e = c.tid + 256 * q;
+          int pp, jj;
+          if (b_kmaj) { jj = e % TN; pp = e / TN; } else { pp = e % TK; jj = e / TK; }
+          const int gj = j0 + jj, gp = p0 + pp;
+          rb[q] = (gj < N && gp < K) ? B.at(gp, gj) : 0.0;
+        }
+      };
+      auto store = [&](int buf) {
+        double* As = sm + buf * 2 * OPS;
+        double* Bs = As + OPS;
+#pragma unroll
+        for (int q = 0; q < AL; ++q) {
+          const int e = c.tid + 256 * q;
+          if (a_kmaj) As[(e / TM) * LK + e % TM] = ra[q];
+          else As[(e / TK) * LM + e % TK] = ra[q];
+        }
+#pragma unroll
+        for (int q = 0; q < BL; ++q) {
+          const int e = c.tid + 256 * q;
+          if (b_kmaj) Bs[(e / TN) * LK + e % TN] = rb[q];
+          else Bs[(e / TK) * LM + e % TK] = rb[q];
+        }
+      };
+      __syncthreads();   // previous tile's readers of both buffers are done
+      load(kbeg);
+      store(0);
+      __syncthreads();
+      int buf = 0;
+      for (int p0 = kbeg; p0 < K; p0 += TK) {
+        const bool more = p0 + TK < K;
+        if (more) load(p0 + TK);
+        const double* As = sm + buf * 2 * OPS;
+        const double* Bs = As + OPS;
+#pragma unroll
+        for (int ks = 0; ks < TK; ks += 4) {
+          double fa[4], fb[NT];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int ii = wm * 32 + 8 * t + ar, pp = ks + ac;
+            fa[t] = a_kmaj ? As[pp * LK + ii] : As[ii * LM + pp];
+          }
+#pragma unroll
+          for (int u = 0; u < NT; ++u) {
+            const int jj = wn * WN + 8 * u + ar, pp = ks + ac;
+            fb[u] = b_kmaj ? Bs[pp * LK + jj] : Bs[jj * LM + pp];
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int u = 0; u < NT; ++u)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                           : "+d"(acc[t][u][0]), "+d"(acc[t][u][1])
+                           : "d"(fa[t]), "d"(fb[u]));
+        }
+        if (more) store(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int gi = i0 + wm * 32 + 8 * t + ar;
+        if (gi >= M) continue;
+#pragma unroll
+        for (int u = 0; u < NT; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gj = j0 + wn * WN + 8 * u + 2 * ac + h;
+            if (gj >= N) continue;
+            double* cp = C + gi * crs + gj * ccs;
+            *cp = (beta == 0.0) ? alpha * acc[t][u][h] : fma(alpha, acc[t][u][h], beta * (*cp));
+          }
+      }
+    }
+  }
+  __syncthreads();
+#else
+  (void)ktri;
+  gemm_t<64>(c, M, N, K, alpha, A, B, beta, C, crs, ccs, sm);
+#endif
+}
+
+#if ENGINE_DEVICE
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// W (jb x nc, row-major ld nc) = V^T C for tall V (mr x jb, col-major ld ldv)
+// and C (mr x nc, col-major ld ldc), jb <= 8*JT.  Split-K over warps: each
+// warp streams its own contiguous row range straight from global memory
+// into DMMA fragments (no SMEM staging, no barriers in the loop, 2 row
+// steps in flight), accumulating a 32 x 8*JT block of W^T; the 8 partial
+// blocks are then summed in a fixed tree order through SMEM (4096 doubles).
+template <int JT>
+__device__ __noinline__ void gemm_vtc_dev(const Ctx& c, int64_t mr, int jb, int nc, const double* V, int64_t ldv,
+                                          const double* C, int64_t ldc, double* W, double* sm) {
+  const int warp = c.tid >> 5, lane = c.tid & 31, ar = lane >> 2, ac = lane & 3;
+  const int64_t steps = (mr + 3) / 4;
+  const int64_t s0 = steps * warp / 8, s1 = steps * (warp + 1) / 8;
+  for (int i0 = 0; i0 < nc; i0 += 32) {
+    double acc[4][JT][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int u = 0; u < JT; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+    const double* cp[4];
+    const double* vp[JT];
+    bool cv[4], vv[JT];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int i = i0 + 8 * t + ar;
+      cv[t] = i < nc;
+      cp[t] = C + (int64_t)(cv[t] ? i : 0) * ldc + ac;
+    }
+#pragma unroll
+    for (int u = 0; u < JT; ++u) {
+      const int j = 8 * u + ar;
+      vv[u] = j < jb;
+      vp[u] = V + (int64_t)(vv[u] ? j : 0) * ldv + ac;
+    }
+    int64_t s = s0;
+    for (; s + 2 <= s1; s += 2) {
+      const int64_t r = 4 * s;
+      double fa[2][4], fb[2][JT];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t rr = r + 4 * h;
+        const bool ok = rr + ac < mr;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) fa[h][t] = (cv[t] && ok) ? cp[t][rr] : 0.0;
+#pragma unroll
+        for (int u = 0; u < JT; ++u) fb[h][u] = (vv[u] && ok) ? vp[u][rr] : 0.0;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int u = 0; u < JT; ++u) dmma(acc[t][u][0], acc[t][u][1], fa[h][t], fb[h][u]);
+    }
+    for (; s < s1; ++s) {
+      const int64_t rr = 4 * s;
+      const bool ok = rr + ac < mr;
+      double fa[4], fb[JT];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) fa[t] = (cv[t] && ok) ? cp[t][rr] : 0.0;
+#pragma unroll
+      for (int u = 0; u < JT; ++u) fb[u] = (vv[u] && ok) ? vp[u][rr] : 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < JT; ++u) dmma(acc[t][u][0], acc[t][u][1], fa[t], fb[u]);
+    }
+    // fixed-order tree reduction of the 8 warp partials (4 -> 2 -> 1 rounds)
+    constexpr int PS = 4 * JT * 2 * 32;   // doubles per warp partial
+    for (int half = 4; half >= 1; half >>= 1) {
+      __syncthreads();
+      if (warp >= half && warp < 2 * half) {
+        double* dst = sm + (warp - half) * PS;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int u = 0; u < JT; ++u) {
+            dst[((t * JT + u) * 2 + 0) * 32 + lane] = acc[t][u][0];
+            dst[((t * JT + u) * 2 + 1) * 32 + lane] = acc[t][u][1];
+          }
+      }
+      __syncthreads();
+      if (warp < half) {
+        const double* src = sm + warp * PS;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int u = 0; u < JT; ++u) {
+            acc[t][u][0] += src[((t * JT + u) * 2 + 0) * 32 + lane];
+            acc[t][u][1] += src[((t * JT + u) * 2 + 1) * 32 + lane];
+          }
+      }
+    }
+    if (warp == 0) {
+      // acc[t][u][h] = W^T(i = i0 + 8t + ar, j = 8u + 2ac + h)
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < JT; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = i0 + 8 * t + ar, j = 8 * u + 2 * ac + h;
+            if (i < nc && j < jb) W[(int64_t)j * nc + i] = acc[t][u][h];
+          }
+    }
+  }
+  __syncthreads();
+}
+
+// C (mr x nc, col-major ld ldc) -= V (mr x jb, col-major ld ldv) W2 (jb x nc,
+// row-major ld nc), jb <= 4*KS.  W2 is staged in SMEM in column chunks of
+// 192 (ld 196: conflict-free B fragments); warps stream 8-row blocks of C
+// and V straight from global memory, C fragments are loaded into the
+// accumulators, updated with -V fragments and stored back.
+template <int KS>
+__device__ __noinline__ void gemm_cmvw_dev(const Ctx& c, int64_t mr, int jb, int nc, const double* V, int64_t ldv,
+                                           const double* W2, double* C, int64_t ldc, double* sm) {
+  constexpr int CH = 192, LDW = 196;
+  const int warp = c.tid >> 5, lane = c.tid & 31, ar = lane >> 2, ac = lane & 3;
+  const int64_t nblk = (mr + 7) / 8;
+  for (int n0 = 0; n0 < nc; n0 += CH) {
+    const int nw = imin(CH, nc - n0);
+    __syncthreads();
+    for (int e = c.tid; e < 4 * KS * LDW; e += 256) {
+      const int k = e / LDW, j = e % LDW;
+      sm[e] = (k < jb && j < nw) ? W2[(int64_t)k * nc + n0 + j] : 0.0;
+    }
+    __syncthreads();
+    for (int64_t b = warp; b < nblk; b += 8) {
+      const int64_t row = 8 * b + ar;
+      const bool rv = row < mr;
+      double fa[KS];
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        const int k = 4 * s + ac;
+        fa[s] = (rv && k < jb) ? -V[row + (int64_t)k * ldv] : 0.0;
+      }
+      for (int j0 = 0; j0 < nw; j0 += 32) {
+        double acc[4][2];
+        double* cp[4][2];
+        bool ok[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = j0 + 8 * q + 2 * ac + h;
+            ok[q][h] = rv && j < nw;
+            cp[q][h] = C + row + (int64_t)(n0 + (ok[q][h] ? j : 0)) * ldc;
+            acc[q][h] = ok[q][h] ? *cp[q][h] : 0.0;
+          }
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            dmma(acc[q][0], acc[q][1], fa[s], sm[(4 * s + ac) * LDW + j0 + 8 * q + ar]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (ok[q][h]) *cp[q][h] = acc[q][h];
+      }
+    }
+  }
+  __syncthreads();
+}
+#endif
+
 // CTA reduction of a small vector (nv <= 33): every thread passes its
 // partials in v[]; the totals are written to out[] (shared) and returned
 // after a barrier.  Deterministic order.
@@ -216,8 +526,21 @@ HDN int apply_block(const Ctx& c, Arena& ar, const double* Vc, int m, int j0, in
   double *W, *W2;
   ALLOC(W, double, (int64_t)jb * nc, ar);
   ALLOC(W2, double, (int64_t)jb * nc, ar);
-  // W = V^T C   (jb x nc): A(i,p) = Vc[p + i*mr], B(p,j) = C[j0+p + j*ldc]
-  gemm_t<32>(c, jb, nc, (int)mr, 1.0, Mat{Vc, mr, 1}, Mat{Cm + j0, 1, ldc}, 0.0, W, nc, 1, sm);
+#if ENGINE_DEVICE
+  if (c.nt == 256) {
+    if (jb <= 8) gemm_vtc_dev<1>(c, mr, jb, nc, Vc, mr, Cm + j0, ldc, W, sm);
+    else gemm_vtc_dev<4>(c, mr, jb, nc, Vc, mr, Cm + j0, ldc, W, sm);
+    if (trans) gemm_t<32>(c, jb, nc, jb, 1.0, Mat{T, NB, 1}, Mat{W, nc, 1}, 0.0, W2, nc, 1, sm);
+    else gemm_t<32>(c, jb, nc, jb, 1.0, Mat{T, 1, NB}, Mat{W, nc, 1}, 0.0, W2, nc, 1, sm);
+    if (jb <= 8) gemm_cmvw_dev<2>(c, mr, jb, nc, Vc, mr, W2, Cm + j0, ldc, sm);
+    else gemm_cmvw_dev<8>(c, mr, jb, nc, Vc, mr, W2, Cm + j0, ldc, sm);
+    ar.release(mk);
+    return OK;
+  }
+#endif
+  // W = V^T C   (jb x nc), computed as W^T = C^T V (nc x jb) so the DMMA
+  // tile's long side runs along nc: A(i,p) = C[j0+p + i*ldc], B(p,j) = Vc[p + j*mr]
+  gemm_dm<32>(c, nc, jb, (int)mr, 1.0, Mat{Cm + j0, ldc, 1}, Mat{Vc, 1, mr}, 0.0, W, 1, nc, sm);
   // W2 = T^op W: T(p,q) at T[p + q*NB]; T^T(p,q) = T[q + p*NB]
   if (trans) gemm_t<32>(c, jb, nc, jb, 1.0, Mat{T, NB, 1}, Mat{W, nc, 1}, 0.0, W2, nc, 1, sm);
   else gemm_t<32>(c, jb, nc, jb, 1.0, Mat{T, 1, NB}, Mat{W, nc, 1}, 0.0, W2, nc, 1, sm);
@@ -231,27 +554,83 @@ HDN int apply_block(const Ctx& c, Arena& ar, const double* Vc, int m, int j0, in
   fprintf(stderr, "\n");
 #endif
   // C -= V W2
-  gemm_t<64>(c, (int)mr, nc, jb, -1.0, Mat{Vc, 1, mr}, Mat{W2, nc, 1}, 1.0, Cm + j0, 1, ldc, sm);
+  gemm_dm<64>(c, (int)mr, nc, jb, -1.0, Mat{Vc, 1, mr}, Mat{W2, nc, 1}, 1.0, Cm + j0, 1, ldc, sm);
   ar.release(mk);
   return OK;
 }
 
+// T factor of a block of jb reflectors from their Gram matrix G = V^T V
+// (jb x jb, row-major) -- dlarft's recurrence T(0:j, j) = -tau_j T(0:j, 0:j)
+// V(:, 0:j)^T v_j with the dot products read from G.  Leader-only, ld NB.
+HD void t_from_gram(const Ctx& c, const double* G, int jb, const double* tau, double* T) {
+  if (c.leader()) {
+    for (int j = 0; j < jb; ++j) {
+      const double t = tau[j];
+      for (int p = 0; p < j; ++p) {
+        double s = 0.0;
+        for (int q = p; q < j; ++q) s += T[p + q * NB] * G[q * jb + j];
+        T[p + j * NB] = -t * s;
+      }
+      T[j + j * NB] = t;
+      for (int p = j + 1; p < NB; ++p) T[p + j * NB] = 0.0;
+    }
+  }
+  c.sync();
+}
+
 // Blocked QR of A (m x n, col-major lda).  Ts: ceil(min(m,n)/NB) * NB*NB.
+// Two-level blocking: each NB-column panel is factored as NS-column
+// sub-panels (level-2) whose block reflectors update the rest of the panel
+// with GEMMs, so a tall panel is streamed ~3x instead of ~NB times; the
+// panel's T comes from one Gram GEMM of its explicit V (which the trailing
+// update needs anyway).
+constexpr int NS = 8;
 HDN int geqrf_nb(const Ctx& c, Arena& ar, double* A, int64_t lda, int m, int n, double* tau, double* Ts,
                  double* sm) {
   const int k = imin(m, n);
   for (int j0 = 0; j0 < k; j0 += NB) {
     const int jb = imin(NB, k - j0);
     double* T = Ts + (int64_t)(j0 / NB) * NB * NB;
-    qr_panel_nb(c, A, lda, m, j0, jb, tau, T, sm);
-    if (j0 + jb < n) {
-      size_t mk = ar.mark();
-      double* Vc;
-      ALLOC(Vc, double, (int64_t)(m - j0) * jb, ar);
-      copy_v(c, A, lda, m, j0, jb, Vc);
-      CK(apply_block(c, ar, Vc, m, j0, jb, T, true, A + (int64_t)(j0 + jb) * lda, lda, n - (j0 + jb), sm));
-      ar.release(mk);
+    const int64_t mr = m - j0;
+    size_t mk = ar.mark();
+    if (mr <= 2048 || jb <= NS) {
+      PROF(c, 16);
+      qr_panel_nb(c, A, lda, m, j0, jb, tau, T, sm);
+    } else {
+      PROF(c, 16);
+      double *Ts_, *Vs;
+      ALLOC(Ts_, double, NB * NB, ar);
+      ALLOC(Vs, double, mr * NS, ar);
+      for (int s0 = 0; s0 < jb; s0 += NS) {
+        const int sb = imin(NS, jb - s0);
+        qr_panel_nb(c, A, lda, m, j0 + s0, sb, tau, Ts_, sm);
+        if (s0 + sb < jb) {
+          copy_v(c, A, lda, m, j0 + s0, sb, Vs);
+          CK(apply_block(c, ar, Vs, m, j0 + s0, sb, Ts_, true, A + (int64_t)(j0 + s0 + sb) * lda, lda,
+                         jb - s0 - sb, sm));
+        }
+      }
     }
+    const bool trail = j0 + jb < n;
+    if (trail || !(mr <= 2048 || jb <= NS)) {
+      PROF(c, 17);
+      double *Vc, *G;
+      ALLOC(Vc, double, mr * jb, ar);
+      copy_v(c, A, lda, m, j0, jb, Vc);
+      if (!(mr <= 2048 || jb <= NS)) {
+        ALLOC(G, double, jb * jb, ar);
+        // G = V^T V: A(i,p) = Vc[p + i*mr], B(p,j) = Vc[p + j*mr]
+#if ENGINE_DEVICE
+        if (c.nt == 256) gemm_vtc_dev<4>(c, mr, jb, jb, Vc, mr, Vc, mr, G, sm);
+        else
+#endif
+        gemm_dm<32>(c, jb, jb, (int)mr, 1.0, Mat{Vc, mr, 1}, Mat{Vc, 1, mr}, 0.0, G, jb, 1, sm);
+        t_from_gram(c, G, jb, tau + j0, T);
+      }
+      if (trail)
+        CK(apply_block(c, ar, Vc, m, j0, jb, T, true, A + (int64_t)(j0 + jb) * lda, lda, n - (j0 + jb), sm));
+    }
+    ar.release(mk);
   }
   return OK;
 }

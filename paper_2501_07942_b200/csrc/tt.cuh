@@ -765,6 +765,7 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
   c.sync();
   const double eps2 = eps_abs * eps_abs;
   int p = 0;
+  int64_t t_rrqr = clk();
   for (int j = 0; j < kmax; ++j) {
     // remaining energy and pivot
     double part = 0.0;
@@ -837,6 +838,13 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
     c.sync();
     p = j + 1;
   }
+  if (c.prof && c.leader()) {
+    c.prof[21] += clk() - t_rrqr;
+    c.prof[22] += p;            // rank reached by the pivoted QR (sum)
+    c.prof[23] += 1;            // svd_rrqr calls
+    if (p > c.prof[24]) c.prof[24] = p;
+    if (p > 64) c.prof[28] += 1;
+  }
   if (p == 0) {   // zero matrix: one zero singular triplet
     for (int64_t e = c.tid; e < m; e += c.nt) U[e] = (e == 0) ? 1.0 : 0.0;
     for (int64_t e = c.tid; e < n; e += c.nt) Vt[e] = (e == 0) ? 1.0 : 0.0;
@@ -847,6 +855,10 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
     return OK;
   }
   // Bt = (R P^T)^T: n x p col-major, Bt[perm[q], i] = R[i, q] (i <= q)
+  int64_t t_sec = clk();
+  auto sec = [&](int cat) {
+    if (c.prof && c.leader()) { const int64_t t1 = clk(); c.prof[cat] += t1 - t_sec; t_sec = t1; }
+  };
   double *Bt, *tq, *Tq, *Z, *Vj, *tmp;
   int* jp;
   ALLOC(Bt, double, (int64_t)n * p, ar);
@@ -870,7 +882,9 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
   ALLOC(tmp, double, p, ar);
   ALLOC(jp, int, p, ar);
   c.sync();
+  sec(27);
   CK(svd_jacobi(c, Z, p, p, p, Vj, s, jp, tmp));
+  sec(25);
   // U = Q1 [Uz[:, perm]; 0]   (m x p);  Q1 = H_0 .. H_{p-1} of the pivoted QR
   for (int64_t e = c.tid; e < (int64_t)m * p; e += c.nt) {
     const int i = (int)(e % m), j = (int)(e / m);
@@ -901,6 +915,7 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
 #endif
     c.sync();
   }
+  sec(26);
   // Vt[i, :] = (Q2 [Vj[:, jp[i]]; 0])^T
   double* Vm;
   ALLOC(Vm, double, (int64_t)n * p, ar);
@@ -915,6 +930,8 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
     Vt[e] = Vm[q + (int64_t)i * n];
   }
   c.sync();
+  sec(27);
+  if (c.prof && c.leader() && p > 64) c.prof[29] += clk() - t_rrqr;
   ar.release(mk);
   *U_out = U;
   *s_out = s;
@@ -972,12 +989,20 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
       Rm[e] = (i <= j) ? w.c[k][i + (int64_t)j * m] : 0.0;
     }
     const int rpp = w.r[k - 1], np_ = w.n[k - 1];
-    ALLOC(nc, double, (int64_t)rpp * np_ * kk, ar);
+    // core k-1 <- core k-1 x_3 R^T : (rpp*n', rl) @ R^T (rl x kk), in place
+    // by row blocks (output row x lands at x*kk <= x*rl, so a block only
+    // overwrites rows already consumed).  R is upper triangular: ktri.
+    const int64_t rows = (int64_t)rpp * np_;
+    const int rb = (int)lmin(rows, lmax(64, ((int64_t)1 << 20) / imax(kk, 1) / 64 * 64));
+    ALLOC(nc, double, (int64_t)rb * kk, ar);
     c.sync();
-    // core k-1 <- core k-1 x_3 R^T : (rpp*n', rl) @ R^T (rl x kk)
-    gemm_t<64>(c, rpp * np_, kk, rl, 1.0, Mat{w.c[k - 1], rl, 1}, Mat{Rm, 1, rl}, 0.0, nc, kk, 1, sm);
-    par_copy(c, w.c[k - 1], nc, (int64_t)rpp * np_ * kk);
-    c.sync();
+    PROF(c, 18);
+    for (int64_t x0 = 0; x0 < rows; x0 += rb) {
+      const int nr = (int)lmin(rb, rows - x0);
+      gemm_dm<64>(c, nr, kk, rl, 1.0, Mat{w.c[k - 1] + x0 * rl, rl, 1}, Mat{Rm, 1, rl}, 0.0, nc, kk, 1, sm, true);
+      par_copy(c, w.c[k - 1] + x0 * kk, nc, (int64_t)nr * kk);
+      c.sync();
+    }
     w.r[k] = kk;
     ar.release(mk);
   }
@@ -1027,7 +1052,10 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
       for (int q = 0; q < m * rprev; ++q) fprintf(stderr, " %.4f", Y[q]);
       fprintf(stderr, "\n");
 #endif
-      CK(apply_q(c, ar, w.c[k], m, m, kk, Ts[k], false, Y, m, rprev, sm));
+      {
+        PROF(c, 19);
+        CK(apply_q(c, ar, w.c[k], m, m, kk, Ts[k], false, Y, m, rprev, sm));
+      }
 #if defined(ENGINE_HOSTSIM) && defined(ENGINE_TRACE)
       fprintf(stderr, "LR k=%d A:", k);
       for (int q = 0; q < m * kk; ++q) fprintf(stderr, " %.4f", w.c[k][q]);
@@ -1133,6 +1161,7 @@ HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double to
     CK(tt_alloc(ar, P, d, n, r));
   }
   for (int k = 0; k < d; ++k) {
+    PROF(c, 20);
     const int n = K.n[k];
     const int nh = (n - 1) / 2;   // n odd
     size_t mk = ar.mark();
@@ -1183,35 +1212,35 @@ HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double to
     }
     c.sync();
     // product fibre (a1 a2, j, b1 b2) = (1/n) [P0 + 2 sum_{om=1..nh} Re(P_om e^{+i 2pi om j/n})]
-    const int64_t nfib = (int64_t)ka * wa * kb * wb;
-    const double inv_n = 1.0 / (double)n;
+    // as a real GEMM per output row (a1 a2):  out (pr x n) = [Re P | Im P] (pr x 2(nh+1)) @ Tw,
+    // Tw(om, j) = w_om cos(2 pi om j / n) / n,  Tw(nh+1+om, j) = -w_om sin(2 pi om j / n) / n,
+    // w_0 = 1, w_om = 2.  Output row block lands at P[row, j, col] (stride pr along j).
+    const int nk = 2 * (nh + 1);
     const int pr = P.r[k + 1];
-    for (int64_t f = c.tid; f < nfib; f += c.nt) {
-      int64_t q = f;
-      const int b2 = (int)(q % wb); q /= wb;
-      const int b1 = (int)(q % kb); q /= kb;
-      const int a2 = (int)(q % wa); q /= wa;
-      const int a1 = (int)q;
-      const double* kr = Kr + ((int64_t)a1 * kb + b1) * (nh + 1);
-      const double* ki = Ki + ((int64_t)a1 * kb + b1) * (nh + 1);
-      const double* wr = Wr + ((int64_t)a2 * wb + b2) * (nh + 1);
-      const double* wi = Wi + ((int64_t)a2 * wb + b2) * (nh + 1);
-      double pre[80], pim[80];   // nh + 1 <= 80 (n <= 159)
-      for (int om = 0; om <= nh; ++om) {
-        pre[om] = kr[om] * wr[om] - ki[om] * wi[om];
-        pim[om] = kr[om] * wi[om] + ki[om] * wr[om];
+    double *Tw, *Ph;
+    ALLOC(Tw, double, (int64_t)nk * n, ar);
+    ALLOC(Ph, double, (int64_t)pr * nk, ar);
+    for (int e = c.tid; e < nk * n; e += c.nt) {
+      const int p = e / n, j = e % n;
+      const int om = p <= nh ? p : p - (nh + 1);
+      const int qq = (int)(((int64_t)om * j) % n);
+      const double w = (om == 0 ? 1.0 : 2.0) / (double)n;
+      Tw[e] = p <= nh ? w * cs[qq] : -w * sn[qq];
+    }
+    for (int row = 0; row < ka * wa; ++row) {
+      const int a1 = row / wa, a2 = row % wa;
+      for (int64_t e = c.tid; e < (int64_t)pr * (nh + 1); e += c.nt) {
+        const int col = (int)(e / (nh + 1)), om = (int)(e % (nh + 1));
+        const int b1 = col / wb, b2 = col % wb;
+        const int64_t ik = ((int64_t)a1 * kb + b1) * (nh + 1) + om;
+        const int64_t iw = ((int64_t)a2 * wb + b2) * (nh + 1) + om;
+        const double kr = Kr[ik], ki = Ki[ik], wr = Wr[iw], wi = Wi[iw];
+        Ph[(int64_t)col * nk + om] = kr * wr - ki * wi;
+        Ph[(int64_t)col * nk + nh + 1 + om] = kr * wi + ki * wr;
       }
-      const int row = a1 * wa + a2, col = b1 * wb + b2;
-      double* dst = P.c[k] + (int64_t)row * n * pr + col;
-      for (int j = 0; j < n; ++j) {
-        double acc = 0.0;
-        for (int om = 1; om <= nh; ++om) {
-          const int qq = (int)(((int64_t)om * j) % n);
-          acc = fma(pre[om], cs[qq], acc);
-          acc = fma(-pim[om], sn[qq], acc);
-        }
-        dst[(int64_t)j * pr] = (pre[0] + 2.0 * acc) * inv_n;
-      }
+      c.sync();
+      gemm_dm<32>(c, pr, n, nk, 1.0, Mat{Ph, nk, 1}, Mat{Tw, n, 1}, 0.0, P.c[k] + (int64_t)row * n * pr, 1, pr,
+                  sm);
     }
     c.sync();
     ar.release(mk);

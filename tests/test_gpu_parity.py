@@ -50,3 +50,24 @@ def test_large_eval_gpu(golden, cuda, case):
     from scenario_util import check_large_eval, use_backend
     use_backend(cuda)
     check_large_eval(golden, case)
+
+
+@pytest.mark.parametrize("ranks,tol", [((1, 60, 60, 1), 1e-6), ((1, 40, 90, 40, 1), 1e-8), ((1, 130, 70, 1), 1e-10)])
+def test_round_tall_cores_gpu(cuda, ranks, tol):
+    """Tall unfoldings (m = n*r' > 2048): two-level panels, Gram-built T, DMMA
+    trailing updates and the in-place triangular R multiply, against the
+    oracle's numpy rounding (tensor_train.py:327)."""
+    from paper_2501_07942_b200 import tensor_train as G
+    from scenario_util import use_backend
+    use_backend(cuda)
+    rs = np.random.RandomState(sum(ranks))
+    n = 65 if len(ranks) == 4 else 21
+    cores = []
+    for k in range(len(ranks) - 1):
+        core = rs.randn(ranks[k], n, ranks[k + 1])
+        core *= (0.7 ** np.arange(ranks[k + 1]))[None, None, :]   # decaying spectrum -> real truncation
+        cores.append(core)
+    ref = T.round_tt(cores, tol)
+    got = G.tt_round(G.TensorTrain.from_cores(cores), tol)
+    assert got.ranks == T.ranks_of(ref)
+    assert rel(T.to_full(got.numpy_cores()), T.to_full(ref)) <= 1e-11

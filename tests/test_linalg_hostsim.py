@@ -17,7 +17,7 @@ def lib():
 
 
 @pytest.mark.parametrize("m,n,nc", [(5, 2, 2), (40, 10, 3), (100, 33, 5), (6, 1, 1), (20, 50, 4), (300, 70, 7),
-                                    (65, 64, 20)])
+                                    (65, 64, 20), (2100, 40, 3), (3000, 70, 5)])
 def test_qr_and_apply(lib, m, n, nc):
     rs = np.random.RandomState(m * 7 + n)
     A0 = rs.randn(m, n)
