@@ -653,4 +653,32 @@ HDN int apply_q(const Ctx& c, Arena& ar, const double* A, int64_t lda, int m, in
   return OK;
 }
 
+// Y (m x ny, col-major ldy) <- H_0 H_1 ... H_{k-1} Y for reflectors stored
+// LAPACK-style in the columns of A (unit diagonal implied) with scalars tau
+// but no T factors (e.g. the pivoted QR): blocks of NB get their T from a
+// Gram GEMM, then one block-reflector application each (last block first).
+HDN int apply_refl_blocked(const Ctx& c, Arena& ar, const double* A, int64_t lda, int m, int k, const double* tau,
+                           double* Y, int64_t ldy, int ny, double* sm) {
+  const int nblk = (k + NB - 1) / NB;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int j0 = b * NB, jb = imin(NB, k - j0);
+    const int64_t mr = m - j0;
+    size_t mk = ar.mark();
+    double *Vc, *G, *T;
+    ALLOC(Vc, double, mr * jb, ar);
+    ALLOC(G, double, jb * jb, ar);
+    ALLOC(T, double, NB * NB, ar);
+    copy_v(c, A, lda, m, j0, jb, Vc);
+#if ENGINE_DEVICE
+    if (c.nt == 256) gemm_vtc_dev<4>(c, mr, jb, jb, Vc, mr, Vc, mr, G, sm);
+    else
+#endif
+    gemm_dm<32>(c, jb, jb, (int)mr, 1.0, Mat{Vc, mr, 1}, Mat{Vc, 1, mr}, 0.0, G, jb, 1, sm);
+    t_from_gram(c, G, jb, tau + j0, T);
+    CK(apply_block(c, ar, Vc, m, j0, jb, T, false, Y, ldy, ny, sm));
+    ar.release(mk);
+  }
+  return OK;
+}
+
 }  // namespace tg

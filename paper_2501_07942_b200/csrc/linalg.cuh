@@ -435,6 +435,100 @@ HDN int svd_jacobi(const Ctx& c, double* X, int64_t ldx, int m, int n, double* V
   return OK;
 }
 
+#if ENGINE_DEVICE
+// One-sided Jacobi on the columns of Z (m x n, col-major ldz), m <= 32*RL,
+// without accumulating V: one warp per column pair of the round-robin
+// tournament, both columns held in registers (all loads in flight at once).
+// Same rotation formulas, order and stopping rule as svd_jacobi.
+template <int RL>
+__device__ __noinline__ void jacobi_cols_reg(const Ctx& c, double* Z, int64_t ldz, int m, int n) {
+  const int np = n + (n & 1), pairs = np / 2;
+  const int warp = c.tid >> 5, lane = c.tid & 31, nwarps = c.nt >> 5;
+  const double tol = DEPS * sqrt((double)m);
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0;
+    for (int round = 0; round < np - 1; ++round) {
+      for (int pr = warp; pr < pairs; pr += nwarps) {
+        int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (np - 1);
+        int b = 1 + (np - 2 - pr + round) % (np - 1);
+        if (a >= n || b >= n) continue;
+        if (a > b) { const int t = a; a = b; b = t; }
+        double* xa = Z + (int64_t)a * ldz;
+        double* xb = Z + (int64_t)b * ldz;
+        double u[RL], v[RL];
+#pragma unroll
+        for (int q = 0; q < RL; ++q) {
+          const int r = lane + 32 * q;
+          u[q] = r < m ? xa[r] : 0.0;
+          v[q] = r < m ? xb[r] : 0.0;
+        }
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int q = 0; q < RL; ++q) {
+          al = fma(u[q], u[q], al);
+          be = fma(v[q], v[q], be);
+          ga = fma(u[q], v[q], ga);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (ga == 0.0 || al == 0.0 || be == 0.0) continue;
+        const double rel = fabs(ga) / sqrt(al * be);
+        if (rel > off) off = rel;
+        if (rel <= tol) continue;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t);
+        const double sn = cs * t;
+#pragma unroll
+        for (int q = 0; q < RL; ++q) {
+          const int r = lane + 32 * q;
+          if (r < m) {
+            xa[r] = cs * u[q] - sn * v[q];
+            xb[r] = sn * u[q] + cs * v[q];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    off = block_max(c, off);
+    if (off <= tol) break;
+  }
+}
+
+// column norms of Z -> s (sorted descending, stable), perm, columns normalised
+__device__ __noinline__ void jacobi_finish(const Ctx& c, double* Z, int64_t ldz, int m, int n, double* s, int* perm,
+                                           double* tmp) {
+  const int warp = c.tid >> 5, lane = c.tid & 31, nwarps = c.nt >> 5;
+  for (int j = warp; j < n; j += nwarps) {
+    const double* zj = Z + (int64_t)j * ldz;
+    double a = 0.0;
+    for (int r = lane; r < m; r += 32) a = fma(zj[r], zj[r], a);
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) tmp[j] = sqrt(a);
+  }
+  __syncthreads();
+  for (int j = c.tid; j < n; j += c.nt) {
+    const double v = tmp[j];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) rank += (tmp[i] > v || (tmp[i] == v && i < j)) ? 1 : 0;
+    perm[rank] = j;
+    s[rank] = v;
+  }
+  __syncthreads();
+  for (int j = warp; j < n; j += nwarps) {
+    const double nr = tmp[j];
+    if (nr > 0.0) {
+      double* zj = Z + (int64_t)j * ldz;
+      for (int r = lane; r < m; r += 32) zj[r] /= nr;
+    }
+  }
+  __syncthreads();
+}
+#endif
+
 // LAPACK dlaic1: one step of incremental condition estimation.
 // job 1: largest singular value, job 2: smallest.  x has length j, w is the
 // new column's top j entries, gamma its diagonal entry.

@@ -720,10 +720,12 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
 // unreduced block perturbs every singular value by <= eps_abs and the tail
 // energies by <= eps_abs^2, so with eps_abs = 1e-3 * delta the truncation
 // rule of tt_round and the kept subspace are unchanged up to ~1e-3 delta.
-// eps_abs = 0 gives the full SVD.  Outputs as svd_rowmajor with kk = p.
+// eps_abs = 0 gives the full SVD.  s holds all kk = p singular values; only
+// the leading nw = min(want, p) vectors are formed (want = 0: all p):
+// U (m x nw, col-major), Vt (nw x n, row-major).
 // ---------------------------------------------------------------------------
 HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double eps_abs, double** U_out,
-                 double** s_out, double** Vt_out, int* kk_out, double* sm) {
+                 double** s_out, double** Vt_out, int* kk_out, double* sm, int want = 0) {
   PROF(c, 8);
   const int kmax = imin(m, n);
   // outputs sized for the worst case (p <= kmax), allocated first
@@ -859,7 +861,8 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
   auto sec = [&](int cat) {
     if (c.prof && c.leader()) { const int64_t t1 = clk(); c.prof[cat] += t1 - t_sec; t_sec = t1; }
   };
-  double *Bt, *tq, *Tq, *Z, *Vj, *tmp;
+  const int nw = want > 0 ? imin(want, p) : p;   // singular vectors needed by the caller
+  double *Bt, *tq, *Tq, *Z, *tmp, *Uz, *Vw;
   int* jp;
   ALLOC(Bt, double, (int64_t)n * p, ar);
   for (int64_t e = c.tid; e < (int64_t)n * p; e += c.nt) {
@@ -878,56 +881,72 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
     const int i = (int)(e % p), j = (int)(e / p);     // Z(i, j) = R2(j, i)
     Z[e] = (j <= i) ? Bt[j + (int64_t)i * n] : 0.0;
   }
-  ALLOC(Vj, double, (int64_t)p * p, ar);
   ALLOC(tmp, double, p, ar);
   ALLOC(jp, int, p, ar);
+  ALLOC(Uz, double, (int64_t)p * nw, ar);   // top nw left vectors of Z (p x nw)
+  ALLOC(Vw, double, (int64_t)n * nw, ar);   // [Vj_top; 0] (n x nw), then Q2 * that
   c.sync();
   sec(27);
-  CK(svd_jacobi(c, Z, p, p, p, Vj, s, jp, tmp));
-  sec(25);
-  // U = Q1 [Uz[:, perm]; 0]   (m x p);  Q1 = H_0 .. H_{p-1} of the pivoted QR
-  for (int64_t e = c.tid; e < (int64_t)m * p; e += c.nt) {
-    const int i = (int)(e % m), j = (int)(e / m);
-    U[e] = (i < p) ? Z[i + (int64_t)jp[j] * p] : 0.0;
-  }
-  c.sync();
-  for (int jj = p - 1; jj >= 0; --jj) {   // apply H_jj (rows jj..m-1) to all p columns
-    const double* v = A + (int64_t)jj * m;
-    const double t2 = tau[jj];
-    if (t2 == 0.0) continue;
+  bool done = false;
 #if ENGINE_DEVICE
-    for (int q = warp; q < p; q += nwarps) {
-      double* uq = U + (int64_t)q * m;
-      double w = 0.0;
-      for (int r = jj + lane; r < m; r += 32) w = fma(r == jj ? 1.0 : v[r], uq[r], w);
-      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-      w *= t2;
-      for (int r = jj + lane; r < m; r += 32) uq[r] -= w * (r == jj ? 1.0 : v[r]);
+  if (c.nt == 256 && p <= 1024) {
+    // Jacobi without V: Vj's top columns are recovered as Z0^T Uz S^-1
+    // (error eps*|Z|/s_i, times s_i in the truncated product).
+    double* Z0;
+    ALLOC(Z0, double, (int64_t)p * p, ar);
+    par_copy(c, Z0, Z, (int64_t)p * p);
+    c.sync();
+    if (p <= 32) jacobi_cols_reg<1>(c, Z, p, p, p);
+    else if (p <= 64) jacobi_cols_reg<2>(c, Z, p, p, p);
+    else if (p <= 128) jacobi_cols_reg<4>(c, Z, p, p, p);
+    else if (p <= 256) jacobi_cols_reg<8>(c, Z, p, p, p);
+    else if (p <= 512) jacobi_cols_reg<16>(c, Z, p, p, p);
+    else jacobi_cols_reg<32>(c, Z, p, p, p);
+    jacobi_finish(c, Z, p, p, p, s, jp, tmp);
+    for (int64_t e = c.tid; e < (int64_t)p * nw; e += c.nt) {
+      const int i = (int)(e % p), j = (int)(e / p);
+      Uz[e] = Z[i + (int64_t)jp[j] * p];
     }
-#else
-    for (int q = 0; q < p; ++q) {
-      double* uq = U + (int64_t)q * m;
-      double w = 0.0;
-      for (int r = jj; r < m; ++r) w = fma(r == jj ? 1.0 : v[r], uq[r], w);
-      w *= t2;
-      for (int r = jj; r < m; ++r) uq[r] -= w * (r == jj ? 1.0 : v[r]);
+    c.sync();
+    // Vw(0:p, j) = Z0^T Uz(:, j) / s_j
+    gemm_dm<32>(c, p, nw, p, 1.0, Mat{Z0, p, 1}, Mat{Uz, 1, p}, 0.0, Vw, 1, n, sm);
+    for (int64_t e = c.tid; e < (int64_t)n * nw; e += c.nt) {
+      const int i = (int)(e % n), j = (int)(e / n);
+      if (i >= p) Vw[e] = 0.0;
+      else Vw[e] = s[j] > 0.0 ? Vw[e] / s[j] : 0.0;
     }
+    c.sync();
+    done = true;
+  }
 #endif
+  if (!done) {
+    double* Vj;
+    ALLOC(Vj, double, (int64_t)p * p, ar);
+    CK(svd_jacobi(c, Z, p, p, p, Vj, s, jp, tmp));
+    for (int64_t e = c.tid; e < (int64_t)p * nw; e += c.nt) {
+      const int i = (int)(e % p), j = (int)(e / p);
+      Uz[e] = Z[i + (int64_t)jp[j] * p];
+    }
+    for (int64_t e = c.tid; e < (int64_t)n * nw; e += c.nt) {
+      const int i = (int)(e % n), j = (int)(e / n);
+      Vw[e] = (i < p) ? Vj[i + (int64_t)jp[j] * p] : 0.0;
+    }
     c.sync();
   }
-  sec(26);
-  // Vt[i, :] = (Q2 [Vj[:, jp[i]]; 0])^T
-  double* Vm;
-  ALLOC(Vm, double, (int64_t)n * p, ar);
-  for (int64_t e = c.tid; e < (int64_t)n * p; e += c.nt) {
-    const int i = (int)(e % n), j = (int)(e / n);
-    Vm[e] = (i < p) ? Vj[i + (int64_t)jp[j] * p] : 0.0;
+  sec(25);
+  // U = Q1 [Uz; 0]   (m x nw);  Q1 = H_0 .. H_{p-1} of the pivoted QR
+  for (int64_t e = c.tid; e < (int64_t)m * nw; e += c.nt) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    U[e] = (i < p) ? Uz[i + (int64_t)j * p] : 0.0;
   }
   c.sync();
-  CK(apply_q(c, ar, Bt, n, n, p, Tq, false, Vm, n, p, sm));
-  for (int64_t e = c.tid; e < (int64_t)p * n; e += c.nt) {
+  CK(apply_refl_blocked(c, ar, A, m, m, p, tau, U, m, nw, sm));
+  sec(26);
+  // Vt[i, :] = (Q2 [Vj[:, i]; 0])^T  for i < nw
+  CK(apply_q(c, ar, Bt, n, n, p, Tq, false, Vw, n, nw, sm));
+  for (int64_t e = c.tid; e < (int64_t)nw * n; e += c.nt) {
     const int i = (int)(e / n), q = (int)(e % n);
-    Vt[e] = Vm[q + (int64_t)i * n];
+    Vt[e] = Vw[q + (int64_t)i * n];
   }
   c.sync();
   sec(27);
@@ -1085,7 +1104,7 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
     }
     double *U, *s, *Vt;
     int kk;
-    CK(svd_rrqr(c, ar, X, mx, rr, 1e-3 * delta, &U, &s, &Vt, &kk, sm));
+    CK(svd_rrqr(c, ar, X, mx, rr, 1e-3 * delta, &U, &s, &Vt, &kk, sm, cap > 0 ? cap : 0));
     double* tail;
     ALLOC(tail, double, kk, ar);
     int rnew = 0;
