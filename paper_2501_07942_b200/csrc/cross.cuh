@@ -180,7 +180,7 @@ HDN int x_fill_ahat(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XSt
 }
 
 // core k from fibres and the pivot block of bond k+1 (tt_algorithms.py:295-308)
-HDN int x_solve_core(const Ctx& c, Arena& ar, XState& s, int k) {
+HDN int x_solve_core(const Ctx& c, Arena& ar, XState& s, int k, double* sm) {
   const int d = s.d, n = s.n[k];
   const int A = x_left(s, k);
   const int Cc = x_right(s, k);
@@ -202,8 +202,9 @@ HDN int x_solve_core(const Ctx& c, Arena& ar, XState& s, int k) {
   ALLOC(cn, double, r, ar);
   ALLOC(jpvt, int, r, ar);
   // A_ls = ahat^T: (i,j) -> ahat[j][i]; B(i, row) = fib[row*cc + i]
-  CK(lstsq_pivoted(c, s.ahat[k + 1], 1, s.maxr, r, s.fib[k], cc, A * n, s.core[k], cc, W, W2, tau, tau2,
-                   jpvt, cn, nullptr));
+  (void)sm;
+  CK(lstsq_pivoted(c, s.ahat[k + 1], 1, s.maxr, r, s.fib[k], cc, A * n, s.core[k], cc, W, W2, tau, tau2, jpvt,
+                   cn, nullptr));
   ar.release(mk);
   return OK;
 }
@@ -254,8 +255,8 @@ HDN int x_accept(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState
   // left slabs of fibre b (new rows x n_b x right(b)); right slabs of fibre b-1
   CK(x_fill_fib(c, ar, C, spec, s, b, old, old + m, 0, x_right(s, b), sm));
   CK(x_fill_fib(c, ar, C, spec, s, b - 1, 0, x_left(s, b - 1), old, old + m, sm));
-  CK(x_solve_core(c, ar, s, b - 1));
-  CK(x_solve_core(c, ar, s, b));
+  CK(x_solve_core(c, ar, s, b - 1, sm));
+  CK(x_solve_core(c, ar, s, b, sm));
   return OK;
 }
 
@@ -641,7 +642,7 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
   c.sync();
   for (int k = 0; k < d; ++k) CK(x_fill_fib(c, ar, C, spec, s, k, 0, x_left(s, k), 0, x_right(s, k), sm));
   for (int b = 1; b < d; ++b) CK(x_fill_ahat(c, ar, C, spec, s, b, 0, 1, 0, 1, sm));
-  for (int k = 0; k < d; ++k) CK(x_solve_core(c, ar, s, k));
+  for (int k = 0; k < d; ++k) CK(x_solve_core(c, ar, s, k, sm));
 
   // total grid points for the fresh-probe budget (may exceed int64: saturate)
   int64_t prod = 1;

@@ -16,6 +16,7 @@
 namespace tg {
 
 constexpr double DEPS = 2.220446049250313e-16;
+constexpr int X_MAXR_SOLVE = 160;   // max r of lstsq_operator (cross max_rank bound)
 
 // ---------------------------------------------------------------------------
 // GEMM: C[i,j] = alpha * sum_p A(i,p) B(p,j) + beta * C[i,j]
@@ -647,123 +648,84 @@ HD void laic1(int job, int j, const double* x, double sest, const double* w, dou
 
 // ---------------------------------------------------------------------------
 // Least squares  A X = B  with A (r x r), B (r x nrhs): the dgelsy algorithm
-// (QR with column pivoting, rank = largest k with |R_kk| > rcond*|R_00|,
-// min-norm solution for rank-deficient A).  A is copied into `W` (r*r), B is
-// read with B(i,j) at B[i + j*ldb] and the solution written to X(i,j) at
-// X[i + j*ldx] (may alias B).  rcond = eps as scipy's default.
+// (QR with column pivoting, rank by incremental condition estimation with
+// rcond = eps as scipy's default, min-norm solution for rank-deficient A).
+// A(i,j) = A[i*lda_r + j*lda_c]; B(i,j) at B[i + j*ldb]; X(i,j) written at
+// X[i + j*ldx].  The pivoted QR and the rank-deficient second QR run on
+// warp 0 (lanes over columns / rows); right-hand sides are solved one per
+// thread with LAPACK's per-column operation order (an explicit solution
+// operator M with X = M B loses ~cond(A)*eps on these ill-conditioned
+// cross matrices and breaks parity).
 // Workspace: W r*r, W2 r*r, tau r, tau2 r, jpvt r (ints), colnorm r.
 // ---------------------------------------------------------------------------
-HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_c, int r,
-                             const double* B, int64_t ldb, int nrhs, double* X, int64_t ldx,
-                             double* W, double* W2, double* tau, double* tau2, int* jpvt,
-                             double* cn, int* rank_out) {
-  // W(i,j) = A(i,j)
+HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_c, int r, const double* B,
+                      int64_t ldb, int nrhs, double* X, int64_t ldx, double* W, double* W2, double* tau, double* tau2,
+                      int* jpvt, double* cn, int* rank_out) {
   for (int64_t e = c.tid; e < (int64_t)r * r; e += c.nt) {
     int i = (int)(e % r), j = (int)(e / r);
     W[i + (int64_t)j * r] = A[i * lda_r + j * lda_c];
   }
+  for (int j = c.tid; j < r; j += c.nt) jpvt[j] = j;
   c.sync();
-  // serial pivoted Householder QR (r <= a few hundred; leader does it with
-  // the other threads helping on the trailing update)
-  if (c.leader())
-    for (int j = 0; j < r; ++j) jpvt[j] = j;
-  c.sync();
-  for (int j = 0; j < r; ++j) {
-    // column norms of the trailing block
-    for (int q = j + c.tid; q < r; q += c.nt) {
-      double s = 0.0;
-      for (int i = j; i < r; ++i) s = fma(W[i + (int64_t)q * r], W[i + (int64_t)q * r], s);
-      cn[q] = s;
-    }
-    c.sync();
-    if (c.leader()) {
-      int best = j;
-      for (int q = j + 1; q < r; ++q)
-        if (cn[q] > cn[best]) best = q;
+#if ENGINE_DEVICE
+  const bool w0 = c.tid < 32;
+  const int lane = c.tid & 31, L = 32;
+#define WSYNC() __syncwarp()
+#else
+  const bool w0 = true;
+  const int L = 1;
+#define WSYNC() (void)0
+#endif
+  if (w0) {
+#if !ENGINE_DEVICE
+    const int lane = 0;
+#endif
+    for (int j = 0; j < r; ++j) {
+      // column norms of the trailing block (each column summed in order)
+      double bv = -1.0;
+      int bi = r;
+      for (int q = j + lane; q < r; q += L) {
+        double s2 = 0.0;
+        for (int i = j; i < r; ++i) s2 = fma(W[i + (int64_t)q * r], W[i + (int64_t)q * r], s2);
+        cn[q] = s2;
+        if (s2 > bv) { bv = s2; bi = q; }
+      }
+#if ENGINE_DEVICE
+      for (int o = 16; o > 0; o >>= 1) {   // first index of the max
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+#endif
+      const int best = bi;
       if (best != j) {
-        for (int i = 0; i < r; ++i) {
-          double t = W[i + (int64_t)j * r];
+        for (int i = lane; i < r; i += L) {
+          const double t = W[i + (int64_t)j * r];
           W[i + (int64_t)j * r] = W[i + (int64_t)best * r];
           W[i + (int64_t)best * r] = t;
         }
-        int t = jpvt[j]; jpvt[j] = jpvt[best]; jpvt[best] = t;
+        if (lane == 0) { const int t = jpvt[j]; jpvt[j] = jpvt[best]; jpvt[best] = t; }
       }
+      WSYNC();
       double* col = W + (int64_t)j * r;
-      double xn = 0.0;
-      for (int i = j + 1; i < r; ++i) xn = fma(col[i], col[i], xn);
-      double t2, beta, scal;
-      larfg(col[j], sqrt(xn), &t2, &beta, &scal);
-      for (int i = j + 1; i < r; ++i) col[i] *= scal;
-      col[j] = beta;
-      tau[j] = t2;
-    }
-    c.sync();
-    const double t2 = tau[j];
-    const double* v = W + (int64_t)j * r;
-    if (t2 != 0.0) {
-      for (int q = j + 1 + c.tid; q < r; q += c.nt) {
-        double* cq = W + (int64_t)q * r;
-        double w = cq[j];
-        for (int i = j + 1; i < r; ++i) w = fma(v[i], cq[i], w);
-        w *= t2;
-        cq[j] -= w;
-        for (int i = j + 1; i < r; ++i) cq[i] -= w * v[i];
-      }
-    }
-    c.sync();
-  }
-  // rank by incremental condition estimation (dgelsy with rcond = eps)
-  int rank = 0;
-  if (c.leader()) {
-    double* xmin = cn;            // reuse: column norms no longer needed
-    double* xmax = tau2;          // (tau2 is rewritten below if rank-deficient)
-    double smax = fabs(W[0]);
-    double smin = smax;
-    if (smax != 0.0) {
-      rank = 1;
-      xmin[0] = 1.0;
-      xmax[0] = 1.0;
-      while (rank < r) {
-        const int i = rank;
-        const double* col = W + (int64_t)i * r;
-        double sminpr, s1, c1, smaxpr, s2, c2;
-        laic1(2, rank, xmin, smin, col, col[i], &sminpr, &s1, &c1);
-        laic1(1, rank, xmax, smax, col, col[i], &smaxpr, &s2, &c2);
-        if (!(smaxpr * DEPS <= sminpr)) break;
-        for (int q = 0; q < rank; ++q) { xmin[q] *= s1; xmax[q] *= s2; }
-        xmin[rank] = c1;
-        xmax[rank] = c2;
-        smin = sminpr;
-        smax = smaxpr;
-        ++rank;
-      }
-    }
-    c.ired[0] = rank;
-  }
-  c.sync();
-  rank = c.ired[0];
-  c.sync();
-  if (rank_out) *rank_out = rank;
-  // rank-deficient: QR of [R11 R12]^T (r x rank) -> min-norm solution
-  if (rank > 0 && rank < r) {
-    // W2(i, j) = R(j, i) for j < rank, i in [0, r): (r x rank), col-major ld r
-    for (int64_t e = c.tid; e < (int64_t)r * rank; e += c.nt) {
-      int i = (int)(e % r), j = (int)(e / r);
-      W2[i + (int64_t)j * r] = (i >= j) ? W[j + (int64_t)i * r] : 0.0;
-    }
-    c.sync();
-    if (c.leader()) {
-      for (int j = 0; j < rank; ++j) {
-        double* col = W2 + (int64_t)j * r;
+      double t2 = 0.0, beta = 0.0, scal = 0.0;
+      if (lane == 0) {
         double xn = 0.0;
         for (int i = j + 1; i < r; ++i) xn = fma(col[i], col[i], xn);
-        double t2, beta, scal;
         larfg(col[j], sqrt(xn), &t2, &beta, &scal);
-        for (int i = j + 1; i < r; ++i) col[i] *= scal;
-        col[j] = beta;
-        tau2[j] = t2;
-        for (int q = j + 1; q < rank; ++q) {
-          double* cq = W2 + (int64_t)q * r;
+      }
+#if ENGINE_DEVICE
+      t2 = __shfl_sync(0xffffffffu, t2, 0);
+      beta = __shfl_sync(0xffffffffu, beta, 0);
+      scal = __shfl_sync(0xffffffffu, scal, 0);
+#endif
+      for (int i = j + 1 + lane; i < r; i += L) col[i] *= scal;
+      WSYNC();
+      if (lane == 0) { col[j] = beta; tau[j] = t2; }
+      WSYNC();
+      if (t2 != 0.0) {
+        for (int q = j + 1 + lane; q < r; q += L) {
+          double* cq = W + (int64_t)q * r;
           double w = cq[j];
           for (int i = j + 1; i < r; ++i) w = fma(col[i], cq[i], w);
           w *= t2;
@@ -771,17 +733,84 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
           for (int i = j + 1; i < r; ++i) cq[i] -= w * col[i];
         }
       }
+      WSYNC();
     }
-    c.sync();
+    // rank by incremental condition estimation (dgelsy with rcond = eps)
+    int rank = 0;
+    if (lane == 0) {
+      double* xmin = cn;            // reuse: column norms no longer needed
+      double* xmax = tau2;          // (tau2 is rewritten below if rank-deficient)
+      double smax = fabs(W[0]);
+      double smin = smax;
+      if (smax != 0.0) {
+        rank = 1;
+        xmin[0] = 1.0;
+        xmax[0] = 1.0;
+        while (rank < r) {
+          const int i = rank;
+          const double* col = W + (int64_t)i * r;
+          double sminpr, s1, c1, smaxpr, s2, c2;
+          laic1(2, rank, xmin, smin, col, col[i], &sminpr, &s1, &c1);
+          laic1(1, rank, xmax, smax, col, col[i], &smaxpr, &s2, &c2);
+          if (!(smaxpr * DEPS <= sminpr)) break;
+          for (int q = 0; q < rank; ++q) { xmin[q] *= s1; xmax[q] *= s2; }
+          xmin[rank] = c1;
+          xmax[rank] = c2;
+          smin = sminpr;
+          smax = smaxpr;
+          ++rank;
+        }
+      }
+      c.ired[0] = rank;
+    }
+    WSYNC();
+    rank = c.ired[0];
+    // rank-deficient: QR of [R11 R12]^T (r x rank) -> min-norm solution
+    if (rank > 0 && rank < r) {
+      for (int64_t e = lane; e < (int64_t)r * rank; e += L) {
+        const int i = (int)(e % r), j = (int)(e / r);
+        W2[i + (int64_t)j * r] = (i >= j) ? W[j + (int64_t)i * r] : 0.0;
+      }
+      WSYNC();
+      for (int j = 0; j < rank; ++j) {
+        double* col = W2 + (int64_t)j * r;
+        double t2 = 0.0, beta = 0.0, scal = 0.0;
+        if (lane == 0) {
+          double xn = 0.0;
+          for (int i = j + 1; i < r; ++i) xn = fma(col[i], col[i], xn);
+          larfg(col[j], sqrt(xn), &t2, &beta, &scal);
+        }
+#if ENGINE_DEVICE
+        t2 = __shfl_sync(0xffffffffu, t2, 0);
+        beta = __shfl_sync(0xffffffffu, beta, 0);
+        scal = __shfl_sync(0xffffffffu, scal, 0);
+#endif
+        for (int i = j + 1 + lane; i < r; i += L) col[i] *= scal;
+        WSYNC();
+        if (lane == 0) { col[j] = beta; tau2[j] = t2; }
+        WSYNC();
+        for (int q = j + 1 + lane; q < rank; q += L) {
+          double* cq = W2 + (int64_t)q * r;
+          double w = cq[j];
+          for (int i = j + 1; i < r; ++i) w = fma(col[i], cq[i], w);
+          w *= t2;
+          cq[j] -= w;
+          for (int i = j + 1; i < r; ++i) cq[i] -= w * col[i];
+        }
+        WSYNC();
+      }
+    }
   }
-  // per right-hand side: y = Q^T b; solve; permute
-  for (int col = c.tid; col < nrhs; col += c.nt) {
-    double y[160];
-    double* yy = y;
-    // (r <= 150 enforced by the cross: max_rank)
-    for (int i = 0; i < r; ++i) yy[i] = B[i + (int64_t)col * ldb];
+#undef WSYNC
+  c.sync();
+  const int rank = c.ired[0];
+  if (rank_out) *rank_out = rank;
+  // per right-hand side: y = Q^T b; triangular / min-norm solve; permute
+  for (int q = c.tid; q < nrhs; q += c.nt) {
+    double yy[X_MAXR_SOLVE], sol[X_MAXR_SOLVE];
+    for (int i = 0; i < r; ++i) yy[i] = B[i + (int64_t)q * ldb];
     for (int j = 0; j < r; ++j) {
-      double t2 = tau[j];
+      const double t2 = tau[j];
       if (t2 == 0.0) continue;
       const double* v = W + (int64_t)j * r;
       double w = yy[j];
@@ -790,27 +819,26 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
       yy[j] -= w;
       for (int i = j + 1; i < r; ++i) yy[i] -= w * v[i];
     }
-    double sol[160];
     if (rank == 0) {
       for (int i = 0; i < r; ++i) sol[i] = 0.0;
     } else if (rank == r) {
       for (int i = r - 1; i >= 0; --i) {
-        double s = yy[i];
-        for (int q = i + 1; q < r; ++q) s -= W[i + (int64_t)q * r] * sol[q];
-        sol[i] = s / W[i + (int64_t)i * r];
+        double s2 = yy[i];
+        for (int k = i + 1; k < r; ++k) s2 -= W[i + (int64_t)k * r] * sol[k];
+        sol[i] = s2 / W[i + (int64_t)i * r];
       }
     } else {
       // [R11 R12] = L2^T Q2^T with W2 = Q2 L2 (L2 upper, rank x rank)
       // solve L2^T w = y[0:rank] (forward), sol = Q2 [w; 0]
-      double wv[160];
+      double wv[X_MAXR_SOLVE];
       for (int i = 0; i < rank; ++i) {
-        double s = yy[i];
-        for (int q = 0; q < i; ++q) s -= W2[q + (int64_t)i * r] * wv[q];
-        wv[i] = s / W2[i + (int64_t)i * r];
+        double s2 = yy[i];
+        for (int k = 0; k < i; ++k) s2 -= W2[k + (int64_t)i * r] * wv[k];
+        wv[i] = s2 / W2[i + (int64_t)i * r];
       }
       for (int i = 0; i < r; ++i) sol[i] = (i < rank) ? wv[i] : 0.0;
       for (int j = rank - 1; j >= 0; --j) {
-        double t2 = tau2[j];
+        const double t2 = tau2[j];
         if (t2 == 0.0) continue;
         const double* v = W2 + (int64_t)j * r;
         double w = sol[j];
@@ -820,7 +848,7 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
         for (int i = j + 1; i < r; ++i) sol[i] -= w * v[i];
       }
     }
-    for (int i = 0; i < r; ++i) X[jpvt[i] + (int64_t)col * ldx] = sol[i];
+    for (int i = 0; i < r; ++i) X[jpvt[i] + (int64_t)q * ldx] = sol[i];
   }
   c.sync();
   return OK;

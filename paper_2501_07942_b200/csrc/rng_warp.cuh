@@ -3,11 +3,11 @@
 // Every draw sequence the cross makes has bounds that do not depend on the
 // drawn values (integers: shape per column; Floyd: j = pop-size..pop-1 then
 // the shuffle i = size-1..1; tail shuffle: i = pop-1..first).  So a warp can
-// produce the 32-bit PCG64 stream 64 values at a time by jump-ahead
-// (state_{m+k} = A_k state_m + C_k, k = 1..32), evaluate 32 Lemire draws in
-// parallel, and fall back to lane 0 only for the rare rejection.  The final
-// generator state (incl. numpy's buffered high half) is restored from the
-// source state of the last value consumed.
+// address the 32-bit PCG64 stream by position: lane l computes value P + l
+// by jump-ahead (state_{m+k} = A_k state_m + C_k, k = 1..32) from a running
+// base, 32 Lemire draws are evaluated in parallel, and only the rare
+// rejection is resolved one value at a time.  The final generator state
+// (incl. numpy's buffered high half) is that of the last value consumed.
 //
 // On the host emulation the 32 "lanes" are looped; the logic is identical.
 #pragma once
@@ -31,16 +31,8 @@ HD void pcg_make_jump(const Pcg64& g, PcgJump* j) {
   }
 }
 
-constexpr int DB_CAP = 128;
-struct DrawBuf {          // shared memory
-  uint32_t v[DB_CAP];     // pending 32-bit values
-  uint64_t slo[DB_CAP];   // source state (after the 64-bit output they came from)
-  uint64_t shi[DB_CAP];
-  uint32_t half[DB_CAP];  // 0 = low half (high half follows), 1 = high half / buffered
-  int head, count;
-  int last_slot_valid;
-  uint64_t last_lo, last_hi;
-  uint32_t last_half, last_next;
+struct DrawBuf {          // (placeholder: draws are position-addressed, no buffer)
+  int unused;
 };
 
 #if ENGINE_DEVICE
@@ -53,52 +45,6 @@ HD uint64_t xsl_rr(uint64_t hi, uint64_t lo) {
   uint64_t x = hi ^ lo;
   unsigned r = (unsigned)(hi >> 58);
   return (x >> r) | (x << ((64u - r) & 63u));
-}
-
-// Append 64 fresh values (32 outputs) after compacting the buffer.  Warp 0.
-HDN void db_refill(const Ctx& c, DrawBuf* db, uint64_t* base_lo, uint64_t* base_hi, const PcgJump* jt) {
-  // compact: move pending values to the front
-  if (c.leader() || !ENGINE_DEVICE) {
-    if (db->head > 0) {
-      for (int q = 0; q < db->count; ++q) {
-        db->v[q] = db->v[db->head + q];
-        db->slo[q] = db->slo[db->head + q];
-        db->shi[q] = db->shi[db->head + q];
-        db->half[q] = db->half[db->head + q];
-      }
-      db->head = 0;
-    }
-  }
-#if ENGINE_DEVICE
-  __syncwarp();
-#endif
-  const int cnt0 = db->count;
-  const u128 base = (((u128)*base_hi) << 64) | *base_lo;
-  uint64_t last_lo = 0, last_hi = 0;
-  LANE_LOOP(l) {
-    const u128 A = (((u128)jt->a_hi[l]) << 64) | jt->a_lo[l];
-    const u128 C = (((u128)jt->c_hi[l]) << 64) | jt->c_lo[l];
-    const u128 st = A * base + C;
-    const uint64_t slo = (uint64_t)st, shi = (uint64_t)(st >> 64);
-    const uint64_t o = xsl_rr(shi, slo);
-    const int q = cnt0 + 2 * l;
-    db->v[q] = (uint32_t)o;
-    db->v[q + 1] = (uint32_t)(o >> 32);
-    db->slo[q] = slo; db->shi[q] = shi; db->half[q] = 0;
-    db->slo[q + 1] = slo; db->shi[q + 1] = shi; db->half[q + 1] = 1;
-    if (l == 31) { last_lo = slo; last_hi = shi; }
-  }
-#if ENGINE_DEVICE
-  last_lo = __shfl_sync(0xffffffffu, last_lo, 31);
-  last_hi = __shfl_sync(0xffffffffu, last_hi, 31);
-  __syncwarp();
-#endif
-  *base_lo = last_lo;
-  *base_hi = last_hi;
-  if (c.leader() || !ENGINE_DEVICE) db->count = cnt0 + 64;
-#if ENGINE_DEVICE
-  __syncwarp();
-#endif
 }
 
 // Lemire draw from value x with inclusive bound b (b < 2^32-1, b > 0):
@@ -115,59 +61,87 @@ HD bool lemire_try(uint32_t x, uint64_t b, uint64_t* res) {
   return true;
 }
 
-HD void db_pop(DrawBuf* db) {
-  const int q = db->head;
-  db->last_slot_valid = 1;
-  db->last_lo = db->slo[q];
-  db->last_hi = db->shi[q];
-  db->last_half = db->half[q];
-  db->last_next = db->v[q];   // value consumed (numpy keeps it as the stale buffer)
-  db->head++;
-  db->count--;
+// Position-addressed view of the 32-bit numpy stream: value p of the
+// current call is the buffered high half g.u32 (p = 0 when g.has32), else
+// half (p - off) % 2 of 64-bit output o = (p - off) / 2, whose source state
+// is g.s advanced o + 1 steps.  `base` holds g.s advanced `ob` steps; any
+// state within 32 steps of it is one jump-table multiply-add away.  All
+// lanes keep identical copies (uniform updates), so no serial bookkeeping.
+struct StreamPos {
+  u128 g0;          // g.s at entry
+  u128 base;        // g.s advanced ob steps
+  int64_t ob;
+  int off;          // 1 if the call starts with a buffered half
+  uint32_t u32_0;   // that buffered half
+};
+
+HD u128 jump_k(const PcgJump* jt, u128 s, int k) {   // k in [1, 32]
+  const u128 A = (((u128)jt->a_hi[k - 1]) << 64) | jt->a_lo[k - 1];
+  const u128 C = (((u128)jt->c_hi[k - 1]) << 64) | jt->c_lo[k - 1];
+  return A * s + C;
+}
+
+// state after `steps` steps from g0 (steps >= ob), rebasing base forward
+HD u128 sp_state(StreamPos& sp, const PcgJump* jt, int64_t steps) {
+  while (steps - sp.ob > 32) { sp.base = jump_k(jt, sp.base, 32); sp.ob += 32; }
+  return steps == sp.ob ? sp.base : jump_k(jt, sp.base, (int)(steps - sp.ob));
+}
+
+// same, without moving base (per-lane lookahead, steps - ob in [0, 32])
+HD u128 sp_peek(const StreamPos& sp, const PcgJump* jt, int64_t steps) {
+  return steps == sp.ob ? sp.base : jump_k(jt, sp.base, (int)(steps - sp.ob));
+}
+
+HD uint32_t sp_value(const StreamPos& sp, const PcgJump* jt, int64_t p) {
+  if (p < sp.off) return sp.u32_0;
+  const int64_t o = (p - sp.off) >> 1;
+  const u128 st = sp_peek(sp, jt, o + 1);
+  const uint64_t out = xsl_rr((uint64_t)(st >> 64), (uint64_t)st);
+  return ((p - sp.off) & 1) ? (uint32_t)(out >> 32) : (uint32_t)out;
+}
+
+// move base so that value p (and the next 32 values) are peekable
+HD void sp_seek(StreamPos& sp, const PcgJump* jt, int64_t p) {
+  const int64_t o = p < sp.off ? 0 : (p - sp.off) >> 1;
+  while (o - sp.ob > 32) { sp.base = jump_k(jt, sp.base, 32); sp.ob += 32; }
+  if (o > sp.ob) { sp.base = jump_k(jt, sp.base, (int)(o - sp.ob)); sp.ob = o; }
 }
 
 // n bounded draws out[t] = bounded(bound(t)), bound(t) in [0, 2^32-2].
-// All CTA threads call; warp 0 works.  g is updated to the numpy state.
+// All CTA threads call; warp 0 works (32 draws per step, lane l evaluating
+// stream value P + l; the first rejection or zero bound ends the accepted
+// run and is resolved uniformly).  g is left as numpy leaves it.
 template <class Bound>
 HDN void warp_draws(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t n, Bound bound, int64_t* out,
                     DrawBuf* db) {
+  (void)db;
   const bool w0 = !ENGINE_DEVICE || c.tid < 32;
   if (w0 && n > 0) {
-    uint64_t base_lo = g->s_lo, base_hi = g->s_hi;
-    if (c.leader() || !ENGINE_DEVICE) {
-      db->head = 0;
-      db->count = 0;
-      db->last_slot_valid = 0;
-      if (g->has32) {
-        db->v[0] = g->u32;
-        db->slo[0] = g->s_lo;
-        db->shi[0] = g->s_hi;
-        db->half[0] = 1;
-        db->count = 1;
-      }
-    }
-#if ENGINE_DEVICE
-    __syncwarp();
-#endif
+    StreamPos sp;
+    sp.g0 = (((u128)g->s_hi) << 64) | g->s_lo;
+    sp.base = sp.g0;
+    sp.ob = 0;
+    sp.off = g->has32 ? 1 : 0;
+    sp.u32_0 = g->u32;
+    int64_t P = 0;   // stream values consumed
     int64_t t = 0;
     while (t < n) {
-      if (db->count < 40) db_refill(c, db, &base_lo, &base_hi, jt);
+      sp_seek(sp, jt, P);
       const int m = (int)lmin(32, n - t);
-      // parallel phase: lane l draws t+l with value head+l (no rejection assumed)
       unsigned rejmask = 0;
       LANE_LOOP(l) {
         bool rej = false;
-        uint64_t res = 0;
         if (l < m) {
           const uint64_t b = bound(t + l);
-          if (b == 0) rej = true;          // consumes nothing: handle serially
-          else rej = !lemire_try(db->v[db->head + l], b, &res);
+          uint64_t res = 0;
+          if (b == 0) rej = true;          // consumes nothing: handled below
+          else rej = !lemire_try(sp_value(sp, jt, P + l), b, &res);
           if (!rej) out[t + l] = (int64_t)res;
         }
 #if ENGINE_DEVICE
-        rejmask = __ballot_sync(0xffffffffu, rej && l < m);
+        rejmask = __ballot_sync(0xffffffffu, rej);
 #else
-        if (rej && l < m) rejmask |= (1u << l);
+        if (rej) rejmask |= (1u << l);
 #endif
       }
       int f = m;
@@ -179,53 +153,45 @@ HDN void warp_draws(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t n, Bound 
         while (!((rejmask >> f) & 1u)) ++f;
 #endif
       }
-      // accept draws t..t+f-1 (lanes >= f may have written provisional outs; they are redrawn)
-      if (c.leader() || !ENGINE_DEVICE) {
-        for (int q = 0; q < f; ++q) db_pop(db);
+      t += f;
+      P += f;
+      if (f < m) {
+        // draw t: zero bound (no value consumed) or Lemire rejection loop
+        const uint64_t b = bound(t);
+        if (b == 0) {
+          if (c.leader() || !ENGINE_DEVICE) out[t] = 0;
+        } else {
+          while (true) {
+            sp_seek(sp, jt, P);
+            uint64_t res = 0;
+            const bool ok = lemire_try(sp_value(sp, jt, P), b, &res);
+            ++P;
+            if (ok) {
+              if (c.leader() || !ENGINE_DEVICE) out[t] = (int64_t)res;
+              break;
+            }
+          }
+        }
+        t += 1;
       }
 #if ENGINE_DEVICE
       __syncwarp();
 #endif
-      t += f;
-      if (f < m) {
-        // serial draw for index t on lane 0 (rejection or zero bound)
-        bool done = false;
-        while (!done) {
-          if (db->count < 2) db_refill(c, db, &base_lo, &base_hi, jt);
-          if (c.leader() || !ENGINE_DEVICE) {
-            const uint64_t b = bound(t);
-            if (b == 0) {
-              out[t] = 0;
-              done = true;
-            } else {
-              while (db->count > 0) {
-                uint64_t res;
-                const bool ok = lemire_try(db->v[db->head], b, &res);
-                db_pop(db);
-                if (ok) { out[t] = (int64_t)res; done = true; break; }
-              }
-            }
-          }
-#if ENGINE_DEVICE
-          __syncwarp();
-          done = __shfl_sync(0xffffffffu, (int)done, 0);
-          __syncwarp();
-#endif
-        }
-        t += 1;
-      }
     }
-    // restore numpy state from the last consumed value
-    if ((c.leader() || !ENGINE_DEVICE) && db->last_slot_valid) {
-      g->s_lo = db->last_lo;
-      g->s_hi = db->last_hi;
-      if (db->last_half == 0) {   // low half consumed: numpy buffers the high half
-        g->has32 = 1;
-        g->u32 = db->v[db->head];
-      } else {
-        g->has32 = 0;
-        g->u32 = db->last_next;
+    // numpy state after the last consumed value
+    if (P > 0 && P - 1 >= sp.off) {
+      const int64_t o = (P - 1 - sp.off) >> 1;
+      const bool low = ((P - 1 - sp.off) & 1) == 0;
+      const u128 st = sp_state(sp, jt, o + 1);
+      const uint64_t outv = xsl_rr((uint64_t)(st >> 64), (uint64_t)st);
+      if (c.leader() || !ENGINE_DEVICE) {
+        g->s_lo = (uint64_t)st;
+        g->s_hi = (uint64_t)(st >> 64);
+        g->has32 = low ? 1u : 0u;          // low half consumed: high half buffered
+        g->u32 = (uint32_t)(outv >> 32);   // buffered half, or the stale consumed one
       }
+    } else if (P > 0) {                    // only the buffered half was consumed
+      if (c.leader() || !ENGINE_DEVICE) g->has32 = 0;
     }
   }
   c.sync();
@@ -387,24 +353,42 @@ HDN void warp_choice(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t pop, int
     out[t] = (int64_t)v;
   }
   c.sync();
-  // in-order resolution of the rare steps (leader): collided[t] lives in flags bit 0
-  if (c.leader()) {
-    for (int64_t t = 0; t < size; ++t) {
-      if (!(flags[t] & 2)) continue;
-      const uint32_t v = (uint32_t)draws[t];
-      uint64_t h = v & mask;
-      while (keys[h] != v) h = (h + 1) & mask;
-      bool coll = mins[h] < (uint32_t)t;
-      if (!coll && (int64_t)v >= jlo) {
-        const int64_t sidx = (int64_t)v - jlo;
-        coll = sidx < t && (flags[sidx] & 1);
+  // in-order resolution of the rare steps: collided[t] lives in flags bit 0.
+  // Warp 0 finds the flagged steps 32 at a time (ballot); the leader
+  // resolves them in order (each may depend on earlier ones).
+  auto resolve = [&](int64_t t) {
+    const uint32_t v = (uint32_t)draws[t];
+    uint64_t h = v & mask;
+    while (keys[h] != v) h = (h + 1) & mask;
+    bool coll = mins[h] < (uint32_t)t;
+    if (!coll && (int64_t)v >= jlo) {
+      const int64_t sidx = (int64_t)v - jlo;
+      coll = sidx < t && (flags[sidx] & 1);
+    }
+    if (coll) {
+      out[t] = jlo + t;
+      flags[t] |= 1;
+    }
+  };
+#if ENGINE_DEVICE
+  if (c.tid < 32) {
+    for (int64_t t0 = 0; t0 < size; t0 += 32) {
+      const int64_t t = t0 + c.tid;
+      unsigned mk = __ballot_sync(0xffffffffu, t < size && (flags[t] & 2));
+      if (c.leader()) {
+        while (mk) {
+          const int b = __ffs(mk) - 1;
+          mk &= mk - 1;
+          resolve(t0 + b);
+        }
       }
-      if (coll) {
-        out[t] = jlo + t;
-        flags[t] |= 1;
-      }
+      __syncwarp();
     }
   }
+#else
+  for (int64_t t = 0; t < size; ++t)
+    if (flags[t] & 2) resolve(t);
+#endif
   c.sync();
   // Fisher-Yates shuffle of out[0..size): step q swaps i = size-1-q and j = sdraws[q]
   swap_resolve(
