@@ -46,11 +46,11 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--batch", type=int, default=1184)  # filters per GPU (4 per resident CTA slot)
-    p.add_argument("--slots", type=int, default=296)   # resident CTAs: 2 per SM x 148
+    p.add_argument("--batch", type=int, default=2368)  # filters per GPU (8 per resident CTA slot)
+    p.add_argument("--slots", type=int, default=0)     # resident CTAs (0: SMs x ttgbf_ctas_per_sm)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C5")
-    p.add_argument("--ws-mb", type=int, default=384)      # per resident CTA slot
+    p.add_argument("--ws-mb", type=int, default=0)        # per resident CTA slot (0: split free HBM)
     p.add_argument("--big-slots", type=int, default=40)   # overflow workspaces for oversized FFT products
     p.add_argument("--big-mb", type=int, default=1280)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -210,6 +210,14 @@ def run_ours(args):
     cfg = BASELINE_CONFIGS[args.config]
     g, x = cfg["grid"], cfg["cross"]
     B = args.batch
+    from paper_2501_07942_b200 import _abi
+    lib = _abi.load_library()
+    if args.slots <= 0:
+        args.slots = torch.cuda.get_device_properties(local).multi_processor_count * int(lib.ttgbf_ctas_per_sm())
+    if args.ws_mb <= 0:
+        free = torch.cuda.mem_get_info(local)[0]
+        reserve = (args.big_slots * args.big_mb << 20) + B * (1 << 17) * 8 + (8 << 30)
+        args.ws_mb = int(max(128, min(512, (free - reserve) // args.slots >> 20)))
     bcfg = BankConfig(n_per_axis=g["n_per_axis"], sigma_mult=g["sigma_mult"], round_tol=g["round_tol"],
                       round_max_rank=g["round_max_rank"], tol=x["tol"], max_rank=x["max_rank"],
                       rng_seed=x["rng_seed"], ws_bytes=args.ws_mb << 20, state_doubles=1 << 17,
@@ -311,7 +319,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded trajectories, SeedSequence((2024, run, 0)))",
         "config": {"workload": WORKLOAD, "filters_per_gpu": B, "runs": world * B, "parallelism": f"dp{world}",
-                   "workspace_slots": args.slots,
+                   "workspace_slots": args.slots, "workspace_mb_per_slot": args.ws_mb,
                    "l2": "per-filter working sets stream from HBM (batch footprint >> 126 MB L2)",
                    "completed_steps": done_all, "restarts": stats["restarts"], "failed_steps": stats["failed"]},
         "gpu_launches": len(bank.timeline),

@@ -298,6 +298,7 @@ int ttgbf_negative_mass(const ttgbf_tt* hdr, const double* data, int64_t cap, in
 int ttgbf_version(void);
 int ttgbf_block_threads(void);
 int64_t ttgbf_smem_bytes(void);
+int ttgbf_ctas_per_sm(void);   /* resident CTAs per SM the kernels are built for */
 const char* ttgbf_status_string(int status);
 
 #ifdef __cplusplus

@@ -95,6 +95,7 @@ SIGNATURES = {
     "ttgbf_version": [],
     "ttgbf_block_threads": [],
     "ttgbf_smem_bytes": [],
+    "ttgbf_ctas_per_sm": [],
     "ttgbf_status_string": [I32],
 }
 RESTYPES = {"ttgbf_smem_bytes": I64, "ttgbf_status_string": ctypes.c_char_p}

@@ -22,7 +22,7 @@ namespace {
 
 #ifdef __CUDACC__
 template <class F>
-__global__ void __launch_bounds__(BLOCK_THREADS, 2) k_items(F f, int count) {
+__global__ void __launch_bounds__(BLOCK_THREADS, CTAS_PER_SM) k_items(F f, int count) {
   extern __shared__ double smem[];
   const Ctx c = make_ctx(smem, threadIdx.x, blockDim.x);
   if ((int)blockIdx.x < count) f(c, (int)blockIdx.x, smem);
@@ -57,6 +57,7 @@ extern "C" {
 int ttgbf_version(void) { return 1; }
 int ttgbf_block_threads(void) { return BLOCK_THREADS; }
 int64_t ttgbf_smem_bytes(void) { return (int64_t)SMEM_DOUBLES * 8; }
+int ttgbf_ctas_per_sm(void) { return CTAS_PER_SM; }
 
 const char* ttgbf_status_string(int s) {
   switch (s) {

@@ -7,10 +7,17 @@
 namespace tg {
 
 constexpr int SMEM_RED = 64 + 1024;       // reductions + scan buffer (doubles)
-constexpr int SMEM_XBLK = 576;            // XShared (+ draw buffer) + XState (doubles)
+constexpr int SMEM_XBLK = 128;            // XShared + XState (doubles)
 constexpr int SMEM_SCRATCH = 8192;        // gemm tiles / QR / chain evaluation
 constexpr int SMEM_DOUBLES = SMEM_RED + SMEM_XBLK + SMEM_SCRATCH;
 constexpr int BLOCK_THREADS = 256;
+// resident CTAs per SM the kernels are built for (registers <= 64K / (256 *
+// this), SMEM_DOUBLES * 8 + 1 KiB <= 228 KiB / this)
+#ifndef TTGBF_CTAS_PER_SM
+#define TTGBF_CTAS_PER_SM 2
+#endif
+constexpr int CTAS_PER_SM = TTGBF_CTAS_PER_SM;
+static_assert((SMEM_DOUBLES * 8 + 1024) * CTAS_PER_SM <= 228 * 1024, "SMEM too large for CTAS_PER_SM");
 
 static_assert(sizeof(XShared) + sizeof(XState) <= SMEM_XBLK * sizeof(double), "xblk too small");
 
