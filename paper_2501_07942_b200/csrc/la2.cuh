@@ -458,19 +458,21 @@ HDN void qr_panel_nb(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
     const double alpha = col[j];
     double t, beta, scal;
     larfg(alpha, sqrt(red[0]), &t, &beta, &scal);
-    if (c.leader()) {
-      // T(0:jj, jj) = -tau_j T(0:jj, 0:jj) g,  g_q = V(:,q)^T v_j = A[j, q] + scal * dot_q
-      double g[NB];
-      for (int q = 0; q < jj; ++q) g[q] = A[(int64_t)(j0 + q) * lda + j] + scal * red[1 + q];
-      for (int p = 0; p < jj; ++p) {
+    // T(0:jj, jj) = -tau_j T(0:jj, 0:jj) g,  g_q = V(:,q)^T v_j = A[j, q] + scal * dot_q.
+    // Thread p owns row p of T (it reads only row p, written by itself in
+    // earlier columns), so the rows are computed in parallel without barriers.
+    for (int p = c.tid; p < NB; p += c.nt) {
+      double tv;
+      if (p < jj) {
         double s = 0.0;
-        for (int q = p; q < jj; ++q) s += T[p + q * NB] * g[q];
-        T[p + jj * NB] = -t * s;
+        for (int q = p; q < jj; ++q) s += T[p + q * NB] * (A[(int64_t)(j0 + q) * lda + j] + scal * red[1 + q]);
+        tv = -t * s;
+      } else {
+        tv = p == jj ? t : 0.0;   // T is upper triangular
       }
-      T[jj + jj * NB] = t;
-      for (int p = jj + 1; p < NB; ++p) T[p + jj * NB] = 0.0;   // T is upper triangular
-      tau[j] = t;
+      T[p + jj * NB] = tv;
     }
+    if (c.leader()) tau[j] = t;
     // pass 2: scale the reflector, then apply H_j to the rest of the panel
     for (int64_t r = j + 1 + c.tid; r < m; r += c.nt) col[r] *= scal;
     c.sync();
@@ -488,8 +490,7 @@ HDN void qr_panel_nb(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
       }
       block_reduce_vec(c, w, nrem, red + NB);
       // include the unit diagonal row j of v_j, scale by tau
-      if (c.leader())
-        for (int q = 0; q < nrem; ++q) red[NB + q] = t * (red[NB + q] + A[(int64_t)(j + 1 + q) * lda + j]);
+      for (int q = c.tid; q < nrem; q += c.nt) red[NB + q] = t * (red[NB + q] + A[(int64_t)(j + 1 + q) * lda + j]);
       c.sync();
       for (int64_t r = j + c.tid; r < m; r += c.nt) {
         const double vr = (r == j) ? 1.0 : col[r];
@@ -562,17 +563,20 @@ HDN int apply_block(const Ctx& c, Arena& ar, const double* Vc, int m, int j0, in
 // T factor of a block of jb reflectors from their Gram matrix G = V^T V
 // (jb x jb, row-major) -- dlarft's recurrence T(0:j, j) = -tau_j T(0:j, 0:j)
 // V(:, 0:j)^T v_j with the dot products read from G.  Leader-only, ld NB.
+// Row p of T depends only on row p itself (and G), so thread p builds it
+// alone: no barriers inside, same operation order as the serial recurrence.
 HD void t_from_gram(const Ctx& c, const double* G, int jb, const double* tau, double* T) {
-  if (c.leader()) {
+  for (int p = c.tid; p < NB; p += c.nt) {
     for (int j = 0; j < jb; ++j) {
-      const double t = tau[j];
-      for (int p = 0; p < j; ++p) {
+      double tv;
+      if (p < j) {
         double s = 0.0;
         for (int q = p; q < j; ++q) s += T[p + q * NB] * G[q * jb + j];
-        T[p + j * NB] = -t * s;
+        tv = -tau[j] * s;
+      } else {
+        tv = p == j ? tau[j] : 0.0;
       }
-      T[j + j * NB] = t;
-      for (int p = j + 1; p < NB; ++p) T[p + j * NB] = 0.0;
+      T[p + j * NB] = tv;
     }
   }
   c.sync();

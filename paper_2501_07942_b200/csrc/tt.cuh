@@ -180,67 +180,87 @@ HD void axis_cell(const AxisGeom& g, double x, int* cell, double* frac, bool* in
 // Warp-per-point chain with the running row vector held in registers: lane l
 // owns entries l, l+32, ... (S slots); v[a] is broadcast by shuffle and each
 // lane accumulates its output columns from coalesced core-row loads.
-template <int S, class Slice>
+template <int S, int P, class Slice>
 __device__ __forceinline__ void chain_regs(const Ctx& c, const TT& t, int64_t K, Slice& s0, double* out) {
-  Slice s1 = s0;
-  const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
-  for (int64_t p0 = 2 * (int64_t)warp; p0 < K; p0 += 2 * (int64_t)nwarps) {
-    const int64_t p1 = p0 + 1;
-    const bool has1 = p1 < K;
-    double v0[S], v1[S];
+  // P points per warp in flight: P independent load streams per step hide
+  // the L2 latency of the core-row reads (the cores do not fit in L1).
+  Slice sl_[P];
 #pragma unroll
-    for (int q = 0; q < S; ++q) { v0[q] = (q == 0 && lane == 0) ? 1.0 : 0.0; v1[q] = v0[q]; }
-    bool dead0 = false, dead1 = !has1;
+  for (int u = 0; u < P; ++u) sl_[u] = s0;
+  const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
+  for (int64_t p0 = P * (int64_t)warp; p0 < K; p0 += P * (int64_t)nwarps) {
+    double v[P][S];
+    bool dead[P], has[P];
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      has[u] = p0 + u < K;
+      dead[u] = !has[u];
+#pragma unroll
+      for (int q = 0; q < S; ++q) v[u][q] = (q == 0 && lane == 0) ? 1.0 : 0.0;
+    }
     for (int k = 0; k < t.d; ++k) {
       const int rl = t.r[k], rr = t.r[k + 1];
       const int64_t sa = (int64_t)t.n[k] * rr;
-      if (!dead0) dead0 = !s0.prepare(k, p0);
-      if (!dead1) dead1 = !s1.prepare(k, p1);
-      if (dead0 && dead1) break;
-      const double *lo0, *hi0, *lo1, *hi1;
-      double wl0, wh0, wl1, wh1;
-      s0.row(k, &lo0, &hi0, &wl0, &wh0);
-      if (has1) s1.row(k, &lo1, &hi1, &wl1, &wh1);
-      else { lo1 = lo0; hi1 = hi0; wl1 = wl0; wh1 = wh0; }
-      double a0[S], a1[S];
+      bool all_dead = true;
 #pragma unroll
-      for (int q = 0; q < S; ++q) { a0[q] = 0.0; a1[q] = 0.0; }
+      for (int u = 0; u < P; ++u) {
+        if (!dead[u]) dead[u] = !sl_[u].prepare(k, p0 + u);
+        all_dead = all_dead && dead[u];
+      }
+      if (all_dead) break;
+      const double *lo[P], *hi[P];
+      double wl[P], wh[P];
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        if (!dead[u]) sl_[u].row(k, &lo[u], &hi[u], &wl[u], &wh[u]);
+        else { lo[u] = hi[u] = t.c[k]; wl[u] = wh[u] = 0.0; }   // finished / outside: row 0, discarded
+      }
+      double a[P][S];
+#pragma unroll
+      for (int u = 0; u < P; ++u)
+#pragma unroll
+        for (int q = 0; q < S; ++q) a[u][q] = 0.0;
 #pragma unroll
       for (int sl = 0; sl < S; ++sl) {
         if (sl * 32 < rl) {
           const int amax = imin(32, rl - sl * 32);
-          const double* r0 = lo0 + (int64_t)(sl * 32) * sa + lane;
-          const double* r1 = lo1 + (int64_t)(sl * 32) * sa + lane;
-          const double* h0 = hi0 + (int64_t)(sl * 32) * sa + lane;
-          const double* h1 = hi1 + (int64_t)(sl * 32) * sa + lane;
-#pragma unroll 4
+          const double* r[P];
+          const double* h[P];
+#pragma unroll
+          for (int u = 0; u < P; ++u) {
+            r[u] = lo[u] + (int64_t)(sl * 32) * sa + lane;
+            h[u] = hi[u] + (int64_t)(sl * 32) * sa + lane;
+          }
+#pragma unroll 2
           for (int l = 0; l < amax; ++l) {
-            const double va0 = __shfl_sync(0xffffffffu, v0[sl], l);
-            const double va1 = __shfl_sync(0xffffffffu, v1[sl], l);
+            double va[P];
+#pragma unroll
+            for (int u = 0; u < P; ++u) va[u] = __shfl_sync(0xffffffffu, v[u][sl], l);
 #pragma unroll
             for (int q = 0; q < S; ++q) {
               if (q * 32 + lane < rr) {
-                double x0 = r0[q * 32], x1 = r1[q * 32];
-                if (Slice::kBlend) {
-                  x0 = x0 * wl0 + h0[q * 32] * wh0;
-                  x1 = x1 * wl1 + h1[q * 32] * wh1;
+#pragma unroll
+                for (int u = 0; u < P; ++u) {
+                  double x = r[u][q * 32];
+                  if (Slice::kBlend) x = x * wl[u] + h[u][q * 32] * wh[u];
+                  a[u][q] = fma(va[u], x, a[u][q]);
                 }
-                a0[q] = fma(va0, x0, a0[q]);
-                a1[q] = fma(va1, x1, a1[q]);
               }
             }
-            r0 += sa; r1 += sa; h0 += sa; h1 += sa;
+#pragma unroll
+            for (int u = 0; u < P; ++u) { r[u] += sa; h[u] += sa; }
           }
         }
       }
 #pragma unroll
-      for (int q = 0; q < S; ++q) { v0[q] = a0[q]; v1[q] = a1[q]; }
+      for (int u = 0; u < P; ++u)
+#pragma unroll
+        for (int q = 0; q < S; ++q) v[u][q] = a[u][q];
     }
-    const double o0 = __shfl_sync(0xffffffffu, v0[0], 0);
-    const double o1 = __shfl_sync(0xffffffffu, v1[0], 0);
-    if (lane == 0) {
-      out[p0] = dead0 ? 0.0 : o0;
-      if (has1) out[p1] = dead1 ? 0.0 : o1;
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      const double o = __shfl_sync(0xffffffffu, v[u][0], 0);
+      if (lane == 0 && has[u]) out[p0 + u] = dead[u] ? 0.0 : o;
     }
   }
   c.sync();
@@ -252,9 +272,9 @@ HDN void tt_chain_eval(const Ctx& c, const TT& t, int64_t K, Slice slice, double
   int maxr = 1;
   for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
 #if ENGINE_DEVICE
-  if (maxr <= 32) { chain_regs<1>(c, t, K, slice, out); return; }
-  if (maxr <= 64) { chain_regs<2>(c, t, K, slice, out); return; }
-  if (maxr <= 128) { chain_regs<4>(c, t, K, slice, out); return; }
+  if (maxr <= 32) { chain_regs<1, 4>(c, t, K, slice, out); return; }
+  if (maxr <= 64) { chain_regs<2, 2>(c, t, K, slice, out); return; }
+  if (maxr <= 128) { chain_regs<4, 2>(c, t, K, slice, out); return; }
   const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
   double* v = sm + (int64_t)warp * 2 * maxr;
   double* w = v + maxr;
@@ -377,28 +397,32 @@ struct PtsFn {
 };
 
 // ---------------------------------------------------------------------------
-// Core-major TT evaluation for large batches: for each core the points are
-// bucketed by their slice (counting sort), each slice (and its right
-// neighbour for 2-tap interpolation) is staged in SMEM, and one warp
-// advances two points at a time reading the core from SMEM instead of L2.
-// Same arithmetic order as tt_chain_eval (blend, then sum over a ascending).
-// Falls back to tt_chain_eval for small batches or ranks > 64.
+// Core-major TT evaluation for batches: for each core the points are
+// bucketed by their slice (counting sort), the buckets are cut into tiles of
+// 8 points, and each warp takes whole tiles: DMMA (m8n8k4 f64) of the 8
+// running row vectors against the slice (and its right neighbour for 2-tap
+// interpolation), B fragments read straight from the core in global memory
+// (L2-resident), so there is no CTA barrier per slice and warps work on
+// different slices at once.  A row's result depends only on its own A row,
+// so the (atomic) order of points inside a bucket does not change any value.
+// Small batches go through tt_chain_eval.
 // ---------------------------------------------------------------------------
-constexpr int64_t BUCKET_MIN_K = 2048;
+constexpr int64_t BUCKET_MIN_K = 64;
+constexpr int BUCKET_MAXR = 160;
 
 template <class Slice>
 HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice slice, double* out, double* sm) {
   int maxr = 1, maxn = 1;
   for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
   for (int k = 0; k < t.d; ++k) maxn = imax(maxn, t.n[k]);
-  if (maxr > 60 || K < BUCKET_MIN_K || maxn > 1000) {
+  if (maxr > BUCKET_MAXR || K < BUCKET_MIN_K || maxn > 1000) {
     tt_chain_eval(c, t, K, slice, out, sm);
     return OK;
   }
   const int d = t.d;
   const size_t mk = ar.mark();
   double *V0, *V1, *wlv, *whv;
-  int32_t *sid, *perm, *offs;
+  int32_t *sid, *perm;
   uint8_t* dead;
   ALLOC(V0, double, K * maxr, ar);
   ALLOC(V1, double, K * maxr, ar);
@@ -406,12 +430,10 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
   ALLOC(whv, double, K, ar);
   ALLOC(sid, int32_t, K, ar);
   ALLOC(perm, int32_t, K, ar);
-  ALLOC(offs, int32_t, maxn + 2, ar);
   ALLOC(dead, uint8_t, K, ar);
   // core 0 (left rank 1): V0[p, b] = blended slice row
   {
-    const int r1 = t.r[1], n0 = t.n[0];
-    (void)n0;
+    const int r1 = t.r[1];
     for (int64_t p = c.tid; p < K; p += c.nt) {
       int sl;
       double wl, wh;
@@ -428,9 +450,9 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
   c.sync();
   double* Vin = V0;
   double* Vout = V1;
-  int* cur = reinterpret_cast<int*>(sm);          // bucket cursors (maxn + 1 <= 1001 ints)
-  double* A = sm + 512;                          // slice s   (rl x rr <= 60 x 60)
-  double* B = A + 60 * 60;                       // slice s+1 (interpolation); ends at 7712 doubles
+  int* cur = reinterpret_cast<int*>(sm);   // bucket cursors   (n + 1 <= 1001)
+  int* offs = cur + 1024;                  // bucket offsets   (n + 1)
+  int* toffs = offs + 1024;                // tile offsets     (n + 1)
   for (int k = 1; k < d; ++k) {
     const int rl = t.r[k], rr = t.r[k + 1], n = t.n[k];
     for (int q = c.tid; q <= n; q += c.nt) cur[q] = 0;
@@ -451,9 +473,17 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
     }
     c.sync();
     if (c.leader()) {
-      int acc = 0;
-      for (int q = 0; q < n; ++q) { offs[q] = acc; const int h = cur[q]; cur[q] = acc; acc += h; }
+      int acc = 0, tacc = 0;
+      for (int q = 0; q < n; ++q) {
+        const int h = cur[q];
+        offs[q] = acc;
+        toffs[q] = tacc;
+        cur[q] = acc;
+        acc += h;
+        tacc += (h + 7) >> 3;
+      }
       offs[n] = acc;
+      toffs[n] = tacc;
     }
     c.sync();
     for (int64_t p = c.tid; p < K; p += c.nt) {
@@ -467,74 +497,82 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
     c.sync();
     const double* G = t.c[k];
     const int64_t sa = (int64_t)n * rr;
-    for (int sl = 0; sl < n; ++sl) {
-      const int beg = offs[sl], end = offs[sl + 1];
-      if (beg == end) continue;
-      for (int e = c.tid; e < rl * rr; e += c.nt) {
-        const int a = e / rr, bb = e % rr;
-        A[e] = G[a * sa + (int64_t)sl * rr + bb];
-        if (Slice::kBlend) B[e] = (sl + 1 < n) ? G[a * sa + (int64_t)(sl + 1) * rr + bb] : 0.0;
-      }
-      c.sync();
 #if ENGINE_DEVICE
-      {
-        // DMMA tiles: 8 points x 8 output columns, k-steps of 4 over rl.
-        // Fragments (PTX m8n8k4 .f64): A(row=lane/4, col=lane%4),
-        // B(row=lane%4, col=lane/4), C(row=lane/4, cols 2*(lane%4)+{0,1}).
-        const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
-        const int ar = lane >> 2, ac = lane & 3;
-        for (int q0 = beg + 8 * warp; q0 < end; q0 += 8 * nwarps) {
-          const int qa = q0 + ar;
-          const bool rv = qa < end;
-          const int pa = rv ? perm[qa] : perm[q0];
-          const double* vrow = Vin + (int64_t)pa * maxr;
-          const double wl = wlv[pa], wh = whv[pa];
-          for (int n0 = 0; n0 < rr; n0 += 8) {
-            double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-            const int bcol = n0 + ar;
-            for (int k0 = 0; k0 < rl; k0 += 4) {
-              const int ka = k0 + ac;
-              const double af = (rv && ka < rl) ? vrow[ka] : 0.0;
-              const bool bv = ka < rl && bcol < rr;
-              const double bf = bv ? A[ka * rr + bcol] : 0.0;
+    {
+      // Fragments (PTX m8n8k4 .f64): A(row=lane/4, col=lane%4),
+      // B(row=lane%4, col=lane/4), C(row=lane/4, cols 2*(lane%4)+{0,1}).
+      const int nwarps = c.nt >> 5, warp = c.tid >> 5, lane = c.tid & 31;
+      const int ar_ = lane >> 2, ac = lane & 3;
+      const int ntiles = toffs[n];
+      for (int tile = warp; tile < ntiles; tile += nwarps) {
+        int lo_ = 0, hi_ = n;                     // slice: toffs[s] <= tile < toffs[s+1]
+        while (hi_ - lo_ > 1) {
+          const int mid = (lo_ + hi_) >> 1;
+          if (toffs[mid] <= tile) lo_ = mid; else hi_ = mid;
+        }
+        const int sl = lo_;
+        const int q0 = offs[sl] + 8 * (tile - toffs[sl]);
+        const int end = offs[sl + 1];
+        const int qa = q0 + ar_;
+        const bool rv = qa < end;
+        const int pa = perm[rv ? qa : q0];
+        const double* vrow = Vin + (int64_t)pa * maxr;
+        const double wl = wlv[pa], wh = whv[pa];
+        const double* Gs = G + (int64_t)sl * rr;
+        const bool has_hi = sl + 1 < n;
+        for (int n0 = 0; n0 < rr; n0 += 8) {
+          double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+          const int bcol = n0 + ar_;
+#pragma unroll 4
+          for (int k0 = 0; k0 < rl; k0 += 4) {
+            const int ka = k0 + ac;
+            const double af = (rv && ka < rl) ? vrow[ka] : 0.0;
+            const bool bv = ka < rl && bcol < rr;
+            const double* gp = Gs + (int64_t)ka * sa + bcol;
+            const double bf = bv ? gp[0] : 0.0;
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(c0), "+d"(c1) : "d"(af), "d"(bf));
+            if (Slice::kBlend) {
+              const double bf2 = (bv && has_hi) ? gp[rr] : 0.0;
               asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                           : "+d"(c0), "+d"(c1) : "d"(af), "d"(bf));
-              if (Slice::kBlend) {
-                const double bf2 = bv ? B[ka * rr + bcol] : 0.0;
-                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                             : "+d"(e0), "+d"(e1) : "d"(af), "d"(bf2));
-              }
+                           : "+d"(e0), "+d"(e1) : "d"(af), "d"(bf2));
             }
-            if (rv) {
-              const int oc = n0 + 2 * ac;
-              double* orow = Vout + (int64_t)pa * maxr;
-              if (Slice::kBlend) {
-                if (oc < rr) orow[oc] = c0 * wl + e0 * wh;
-                if (oc + 1 < rr) orow[oc + 1] = c1 * wl + e1 * wh;
-              } else {
-                if (oc < rr) orow[oc] = c0;
-                if (oc + 1 < rr) orow[oc + 1] = c1;
-              }
+          }
+          if (rv) {
+            const int oc = n0 + 2 * ac;
+            double* orow = Vout + (int64_t)pa * maxr;
+            if (Slice::kBlend) {
+              if (oc < rr) orow[oc] = c0 * wl + e0 * wh;
+              if (oc + 1 < rr) orow[oc + 1] = c1 * wl + e1 * wh;
+            } else {
+              if (oc < rr) orow[oc] = c0;
+              if (oc + 1 < rr) orow[oc + 1] = c1;
             }
           }
         }
       }
+    }
 #else
-      for (int q0 = beg; q0 < end; ++q0) {
+    for (int sl = 0; sl < n; ++sl) {
+      for (int q0 = offs[sl]; q0 < offs[sl + 1]; ++q0) {
         const int p = perm[q0];
         const double wl = wlv[p], wh = whv[p];
         for (int bb = 0; bb < rr; ++bb) {
           double acc = 0.0, acc2 = 0.0;
           for (int a = 0; a < rl; ++a) {
-            acc = fma(Vin[(int64_t)p * maxr + a], A[a * rr + bb], acc);
-            if (Slice::kBlend) acc2 = fma(Vin[(int64_t)p * maxr + a], B[a * rr + bb], acc2);
+            const double g = G[a * sa + (int64_t)sl * rr + bb];
+            acc = fma(Vin[(int64_t)p * maxr + a], g, acc);
+            if (Slice::kBlend) {
+              const double g2 = (sl + 1 < n) ? G[a * sa + (int64_t)(sl + 1) * rr + bb] : 0.0;
+              acc2 = fma(Vin[(int64_t)p * maxr + a], g2, acc2);
+            }
           }
           Vout[(int64_t)p * maxr + bb] = Slice::kBlend ? acc * wl + acc2 * wh : acc;
         }
       }
-#endif
-      c.sync();
     }
+#endif
+    c.sync();
     double* tmp = Vin; Vin = Vout; Vout = tmp;
   }
   for (int64_t p = c.tid; p < K; p += c.nt) out[p] = dead[p] ? 0.0 : Vin[p * maxr];
