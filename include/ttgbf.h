@@ -26,6 +26,8 @@
  *   ttgbf_greedy_cross        tt_algorithms.greedy_cross        tt_algorithms.py:463-596
  *                             (on the prior / likelihood / kernel black boxes)
  *   ttgbf_negative_mass       filters._negative_mass_tt         filters.py:427-436
+ *   ttgbf_dense_*             filters.dense_fft_pmf_step pieces  filters.py:888-934
+ *                             (the dense FFT PMF on the GPU)
  */
 #ifndef TTGBF_H
 #define TTGBF_H
@@ -300,6 +302,45 @@ int ttgbf_block_threads(void);
 int64_t ttgbf_smem_bytes(void);
 int ttgbf_ctas_per_sm(void);   /* resident CTAs per SM the kernels are built for */
 const char* ttgbf_status_string(int status);
+
+/* ---- dense grid filter: dense_fft_pmf_step (filters.py:888-934) --------
+ * Weights are C-order float64 arrays over the grid `axes` (d <= 8 axes);
+ * complex buffers are interleaved (re, im) float64.  `axes` and `shape` are
+ * HOST arrays (read on the host, the geometry goes to the kernels by value);
+ * every other pointer is device memory.  Each call launches on `stream` and
+ * returns a status. */
+
+/* initial_pmd_dense values N(x - mean; cov) (filters.py:487-494) */
+int ttgbf_dense_prior(const ttgbf_gauss* prior, const ttgbf_axis* axes, int d, double* w, void* stream);
+/* w *= p(z | x) (measurement_update, dense branch, filters.py:564-566) */
+int ttgbf_dense_likelihood(const ttgbf_model* model, const double* z, const ttgbf_axis* axes, int d, double* w,
+                           void* stream);
+/* deterministic sums over the grid into out[]:
+ *   mode 0: {sum max(w,0), sum min(w,0)}           (_finalize_dense, filters.py:439-451)
+ *   mode 1: {sum w*cv, sum_k x_k w*cv}             (moments_from_pmd, filters.py:323-329)
+ *   mode 2: {sum (x_i-m_i)(x_j-m_j) w*cv, i <= j}  (filters.py:330-332)
+ * partials: ttgbf_dense_reduce_blocks() doubles of scratch. */
+int ttgbf_dense_reduce(const double* w, const ttgbf_axis* axes, int d, int mode, double cell_volume,
+                       const double* mean, double* partials, double* out, void* stream);
+int ttgbf_dense_reduce_blocks(void);
+/* w = max(w, 0) / mass (_finalize_dense) */
+int ttgbf_dense_finalize(double* w, int64_t n, double mass, void* stream);
+/* RegularGridInterpolator(old axes, w_old, "linear", fill 0) at the new grid's
+ * nodes mapped by F^-1 (Finv row-major, leading dimension TTGBF_MAXD), written
+ * as complex (filters.py:911-916) */
+int ttgbf_dense_interp(const double* w_old, const ttgbf_axis* old_axes, const ttgbf_axis* new_axes, int d,
+                       const double* Finv, double* out_complex, void* stream);
+/* FFT kernel N(disp; 0, Q) * cell_volume / |det F| on ifftshift
+ * displacements idx * steps, written as complex (filters.py:920-927) */
+int ttgbf_dense_kernel(const ttgbf_model* model, const ttgbf_axis* axes, int d, const double* steps,
+                       double cell_volume, double abs_det_f, double* out_complex, void* stream);
+/* in-place DFT along `axis` (numpy.fft.fftn / ifftn per axis; inverse scales
+ * by 1/n); roots_complex = exp(-2 pi i q / n), q < n (filters.py:732-736) */
+int ttgbf_dense_dft(double* data_complex, const int32_t* shape, int d, int axis, int inverse,
+                    const double* roots_complex, void* stream);
+/* a *= b (complex, n elements); w = Re(a) */
+int ttgbf_dense_cmul(double* a_complex, const double* b_complex, int64_t n, void* stream);
+int ttgbf_dense_real(const double* a_complex, double* w, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

@@ -97,7 +97,19 @@ SIGNATURES = {
     "ttgbf_smem_bytes": [],
     "ttgbf_ctas_per_sm": [],
     "ttgbf_status_string": [I32],
+    # dense grid filter (csrc/dense.cu)
+    "ttgbf_dense_prior": [P, P, I32, P, P],
+    "ttgbf_dense_likelihood": [P, P, P, I32, P, P],
+    "ttgbf_dense_reduce": [P, P, I32, I32, F64, P, P, P, P],
+    "ttgbf_dense_reduce_blocks": [],
+    "ttgbf_dense_finalize": [P, I64, F64, P],
+    "ttgbf_dense_interp": [P, P, P, I32, P, P, P],
+    "ttgbf_dense_kernel": [P, P, I32, P, F64, F64, P, P],
+    "ttgbf_dense_dft": [P, P, I32, I32, I32, P, P],
+    "ttgbf_dense_cmul": [P, P, I64, P],
+    "ttgbf_dense_real": [P, P, I64, P],
 }
+DENSE = frozenset(n for n in SIGNATURES if n.startswith("ttgbf_dense_"))
 RESTYPES = {"ttgbf_smem_bytes": I64, "ttgbf_status_string": ctypes.c_char_p}
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -105,8 +117,12 @@ LIB_DIR = os.path.join(HERE, "_lib")
 PRODUCT_LIB = os.path.join(LIB_DIR, "libttgbf.so")
 
 
-def bind(lib):
+def bind(lib, dense: bool = True):
+    """Set ctypes signatures; every declared symbol must exist (the test-only
+    host emulation of the TT engine passes dense=False: it has no dense TU)."""
     for name, args in SIGNATURES.items():
+        if not dense and name in DENSE:
+            continue
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = RESTYPES.get(name, I32)

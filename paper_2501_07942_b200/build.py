@@ -1,4 +1,10 @@
-"""Build the sm_100a product library in-tree (paper_2501_07942_b200/_lib/libttgbf.so)."""
+"""Build the sm_100a product library in-tree (paper_2501_07942_b200/_lib/libttgbf.so).
+
+Two translation units, compiled in parallel and linked into one library:
+api.cu (the TT step engine; every csrc/*.cuh) and dense.cu (the dense grid
+filter; common.cuh + measure.cuh only).  Objects are rebuilt only when one
+of their sources is newer.
+"""
 
 from __future__ import annotations
 
@@ -10,18 +16,42 @@ import time
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-OUT = os.path.join(HERE, "_lib", "libttgbf.so")
+LIBDIR = os.path.join(HERE, "_lib")
+OUT = os.path.join(LIBDIR, "libttgbf.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+HEADER = os.path.join(ROOT, "include", "ttgbf.h")
 
 FLAGS = [
     "-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-    "--extended-lambda", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
+    "--extended-lambda", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
 ]
 
 
+def _srcs(names):
+    return [os.path.join(CSRC, f) for f in names] + [HEADER]
+
+
+def units():
+    cuh = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
+    return {
+        "api": (os.path.join(CSRC, "api.cu"), _srcs(["api.cu"] + cuh)),
+        "dense": (os.path.join(CSRC, "dense.cu"), _srcs(["dense.cu", "common.cuh", "measure.cuh"])),
+    }
+
+
 def sources():
-    srcs = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith((".cu", ".cuh"))]
-    return srcs + [os.path.join(ROOT, "include", "ttgbf.h")]
+    out = set()
+    for _, deps in units().values():
+        out.update(deps)
+    return sorted(out)
+
+
+def _obj(name):
+    return os.path.join(LIBDIR, f"{name}.o")
+
+
+def _stale(path, deps):
+    return not os.path.exists(path) or os.path.getmtime(path) < max(os.path.getmtime(s) for s in deps)
 
 
 def up_to_date() -> bool:
@@ -33,16 +63,29 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = True) -> str:
     if not force and up_to_date():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    tmp = OUT + ".tmp"
-    cmd = [NVCC] + FLAGS + ["-o", tmp, os.path.join(CSRC, "api.cu")]
+    os.makedirs(LIBDIR, exist_ok=True)
     t0 = time.time()
+    procs = {}
+    for name, (src, deps) in units().items():
+        obj = _obj(name)
+        if force or _stale(obj, deps):
+            cmd = [NVCC] + FLAGS + ["-c", "-o", obj + ".tmp", src]
+            procs[name] = (obj, subprocess.Popen(cmd, cwd=CSRC, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                                                 text=True))
+    for name, (obj, proc) in procs.items():
+        log = proc.communicate()[0]
+        if proc.returncode != 0:
+            sys.stderr.write(log)
+            raise RuntimeError(f"nvcc failed compiling {name}.cu")
+        with open(os.path.join(LIBDIR, f"ptxas_{name}.log"), "w") as f:
+            f.write(log)
+        os.replace(obj + ".tmp", obj)
+    tmp = OUT + ".tmp"
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp] + [_obj(n) for n in units()]
     proc = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
-        raise RuntimeError("nvcc failed building libttgbf.so")
-    with open(os.path.join(os.path.dirname(OUT), "ptxas.log"), "w") as f:
-        f.write(proc.stdout + proc.stderr)
+        raise RuntimeError("nvcc failed linking libttgbf.so")
     os.replace(tmp, OUT)
     if verbose:
         print(f"built {OUT} in {time.time() - t0:.0f}s", flush=True)

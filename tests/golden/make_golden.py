@@ -181,8 +181,44 @@ def trajectories():
     np.savez_compressed(os.path.join(HERE, "trajectories.npz"), **out)
 
 
+def dense():
+    """dense_fft_pmf_step trajectories: radar (d=2, full
+    densities) and the BASELINE config-1 model (d=4, N=33; densities at 10^4
+    seeded indices)."""
+    from paper_2501_07942_b200.configs import SPECS
+    out = {}
+    cases = [("radar", SPECS["radar"], np.array([20.0, 20.0]), np.diag([9.0, 9.0]), 33, 4.0, 5),
+             ("cv4", SPECS["cv4"], np.array([10.0, 10.0, 1.0, 1.0]), np.diag([1.0, 1.0, 0.1, 0.1]), 33, 6.0, 3)]
+    for name, spec, mean, cov, n, sig, steps in cases:
+        m = ref_model(spec)
+        traj = rm.simulate(m, mean, cov, steps, seed=np.random.SeedSequence((2024, 0, 0)))
+        gcfg = rf.GridConfig(n_per_axis=n, sigma_mult=sig, round_tol=1e-8)
+        pmd = rf.initial_pmd_dense(MomentEstimate(mean, cov), gcfg)
+        shape = pmd.weights.shape
+        idx = np.stack([np.random.default_rng(7).integers(0, s, 10000) for s in shape], axis=1)
+        out[f"{name}/idx"] = idx
+        out[f"{name}/z"] = traj.measurements
+        out[f"{name}/init_sample"] = pmd.weights[tuple(idx.T)]
+        if len(shape) == 2:
+            out[f"{name}/init"] = pmd.weights
+        for k in range(steps):
+            pmd = rf.dense_fft_pmf_step(pmd, m, traj.measurements[k], gcfg)
+            dg = pmd.diag
+            out[f"{name}/{k}/filt_mean"] = dg.filt_moments.mean
+            out[f"{name}/{k}/filt_cov"] = dg.filt_moments.cov
+            out[f"{name}/{k}/axes"] = np.stack(pmd.grid.axes)
+            out[f"{name}/{k}/diag"] = np.array([dg.mass_before_norm, dg.clipped_mass, float(dg.outlier),
+                                                float(dg.spd_fixed)])
+            out[f"{name}/{k}/sample"] = pmd.weights[tuple(idx.T)]
+            out[f"{name}/{k}/sum"] = np.array(float(pmd.weights.sum()))
+            if len(shape) == 2:
+                out[f"{name}/{k}/pred"] = pmd.weights
+        out[f"{name}/steps"] = np.array(steps)
+    np.savez_compressed(os.path.join(HERE, "dense.npz"), **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["primitives", "crosses", "models", "trajectories"]
+    which = sys.argv[1:] or ["primitives", "crosses", "models", "trajectories", "dense"]
     for w in which:
         t = time.time()
         globals()[w]()

@@ -53,7 +53,7 @@ class HostBackend:
     def __init__(self):
         from paper_2501_07942_b200 import _abi
         import torch
-        self.lib = _abi.bind(ctypes.CDLL(build()))
+        self.lib = _abi.bind(ctypes.CDLL(build()), dense=False)
         self.stream_ptr = None
         self.torch = torch
         self.device = torch.device("cpu")
