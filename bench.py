@@ -192,6 +192,16 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
+def dram_traffic_per_step():
+    """DRAM bytes per attempted filter step of ttgbf_filter_run, from the committed
+    ncu capture (dram__bytes_read.sum + dram__bytes_write.sum, profiles/)."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_dram_c5.json")
+    if not os.path.exists(path):
+        return None, None
+    rec = json.load(open(path))
+    return float(rec["dram_bytes_per_attempted_step"]), f"profiles/r01_ncu_dram_c5.json ({rec['kernel']}) x attempted steps"
+
+
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
@@ -313,6 +323,13 @@ def run_ours(args):
     dom_time = sum(per_kernel[dom]) / len(per_kernel[dom])
     flops_per_launch = stats["flops"] / max(1, len(per_kernel[dom]))
     achieved = flops_per_launch / dom_time / 1e12
+    per_step, traffic_src = dram_traffic_per_step()
+    attempted = int((recs["status"] >= 0).sum())
+    traffic_per_launch = per_step * attempted / max(1, len(per_kernel[dom])) if per_step else None
+    hbm_peak = None
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        hbm_peak = json.load(open(pk)).get("hbm_gbs")
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
@@ -325,7 +342,11 @@ def run_ours(args):
         "gpu_launches": len(bank.timeline),
         "launch_note": "one persistent ttgbf_filter_run launch runs all K steps of all filters (device geometry)",
         "roofline": {"bound": "tensor", "precision": "fp64", "kernel": dom, "achieved": achieved,
-                     "peak": peak_fp64, "unit": "TFLOP/s", "frac": achieved / peak_fp64, "traffic": None,
+                     "peak": peak_fp64, "unit": "TFLOP/s", "frac": achieved / peak_fp64,
+                     "traffic": traffic_per_launch,
+                     "traffic_source": traffic_src,
+                     "hbm_achieved_gbs": (traffic_per_launch / dom_time / 1e9) if traffic_per_launch and dom_time else None,
+                     "hbm_peak_gbs": hbm_peak,
                      "peak_source": "cuBLAS DGEMM 8192^3 burst measured in this run (MEASURED_PEAKS.json has no FP64)",
                      "algorithmic_flops_per_launch": flops_per_launch, "launch_s": dom_time},
         "kernel_time_s": {k: sum(v) for k, v in per_kernel.items()},

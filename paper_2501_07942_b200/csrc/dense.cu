@@ -216,19 +216,29 @@ __global__ void __launch_bounds__(THREADS) k_kernel(Geo g, const ttgbf_model* m,
 }
 
 // One axis of an n-point DFT over `lines` = outer*inner lines (element j of
-// line (o, i) at (o*n + j)*inner + i).  A CTA stages LT lines in SMEM and
-// each thread forms outputs (omega, line) as a fixed-order sum over j with
-// twiddle root[(omega*j) mod n] (conjugated and scaled by 1/n for ifft).
+// line (o, i) at (o*n + j)*inner + i).  A CTA stages LT lines in SMEM.  For
+// n = n1*n2 (n1 the smallest prime factor) the transform is two-stage
+// Cooley-Tukey in SMEM -- length-n1 DFTs, twiddles W_n^(j2 k1), length-n2
+// DFTs -- so an element costs n1 + n2 + 1 complex MACs instead of n; a
+// prime n is a direct DFT.  Every twiddle is root[(.) mod n] from the host's
+// exp(-2 pi i q / n) table, conjugated and scaled by 1/n for ifft.
 constexpr int LT = 16;
-__global__ void __launch_bounds__(THREADS) k_dft(double2* x, int64_t outer, int n, int64_t inner, int inverse,
+__device__ __forceinline__ void cmac(double& re, double& im, const double2 a, const double2 r) {
+  re = fma(a.x, r.x, fma(-a.y, r.y, re));
+  im = fma(a.x, r.y, fma(a.y, r.x, im));
+}
+
+__global__ void __launch_bounds__(THREADS) k_dft(double2* x, int64_t outer, int n, int n1, int64_t inner, int inverse,
                                                  const double2* roots) {
   extern __shared__ double2 sh[];
-  double2* xs = sh;             // [n][LT]
-  double2* rt = sh + n * LT;    // [n]
+  double2* xs = sh;               // [n][LT]
+  double2* ys = sh + n * LT;      // [n][LT]  stage-1 output
+  double2* rt = ys + n * LT;      // [n]
   for (int q = threadIdx.x; q < n; q += blockDim.x) {
     const double2 r = roots[q];
     rt[q] = inverse ? make_double2(r.x, -r.y) : r;
   }
+  const int n2 = n / n1;
   const int64_t lines = outer * inner;
   const double scale = inverse ? 1.0 / (double)n : 1.0;
   for (int64_t l0 = (int64_t)blockIdx.x * LT; l0 < lines; l0 += (int64_t)gridDim.x * LT) {
@@ -244,17 +254,41 @@ __global__ void __launch_bounds__(THREADS) k_dft(double2* x, int64_t outer, int 
       }
     }
     __syncthreads();
+    const double2* src = xs;
+    int m = n, stride = 1;          // final stage: length m DFT over src rows j*stride (+ k1)
+    if (n1 > 1) {
+      // stage 1: Y[j2*n1 + k1] = W_n^(j2 k1) * sum_j1 W_n1^(j1 k1) x[j2 + n2 j1]
+      for (int e = threadIdx.x; e < n * LT; e += blockDim.x) {
+        const int r = e / LT, l = e % LT;
+        const int j2 = r / n1, k1 = r % n1;
+        double re = 0.0, im = 0.0;
+        int q = 0;
+        const int dq = (k1 * n2) % n;
+        for (int j1 = 0; j1 < n1; ++j1) {
+          cmac(re, im, xs[(j2 + n2 * j1) * LT + l], rt[q]);
+          q += dq;
+          if (q >= n) q -= n;
+        }
+        const double2 t = rt[(j2 * k1) % n];
+        ys[e] = make_double2(re * t.x - im * t.y, re * t.y + im * t.x);
+      }
+      __syncthreads();
+      src = ys;
+      m = n2;
+      stride = n1;
+    }
+    // final stage: X[k1 + n1 k2] = sum_j2 W_n2^(j2 k2) src[j2*n1 + k1]   (n1 = 1: direct DFT)
     for (int e = threadIdx.x; e < n * LT; e += blockDim.x) {
       const int om = e / LT, l = e % LT;
       const int64_t L = l0 + l;
       if (L >= lines) continue;
+      const int k1 = om % stride, k2 = om / stride;
       double re = 0.0, im = 0.0;
       int q = 0;
-      for (int j = 0; j < n; ++j) {
-        const double2 a = xs[j * LT + l], r = rt[q];
-        re = fma(a.x, r.x, fma(-a.y, r.y, re));
-        im = fma(a.x, r.y, fma(a.y, r.x, im));
-        q += om;
+      const int dq = (k2 * stride) % n;
+      for (int j2 = 0; j2 < m; ++j2) {
+        cmac(re, im, src[(j2 * stride + k1) * LT + l], rt[q]);
+        q += dq;
         if (q >= n) q -= n;
       }
       const int64_t o = L / inner, i = L % inner;
@@ -366,14 +400,17 @@ int ttgbf_dense_dft(double* data_complex, const int32_t* shape, int d, int axis,
   for (int k = 0; k < axis; ++k) outer *= shape[k];
   for (int k = axis + 1; k < d; ++k) inner *= shape[k];
   const int n = shape[axis];
-  const size_t smem = (size_t)(n * LT + n) * sizeof(double2);
+  int n1 = 1;                        // smallest prime factor (two-stage transform) or 1 (prime n)
+  for (int p = 2; p * p <= n; ++p)
+    if (n % p == 0) { n1 = p; break; }
+  const size_t smem = (size_t)(2 * n * LT + n) * sizeof(double2);
   if (smem > 200 * 1024) return TTGBF_E_ARG;
   if (cudaFuncSetAttribute(k_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return TTGBF_E_CUDA;
   const int64_t lines = outer * inner;
   const int64_t blocks = (lines + LT - 1) / LT;
   const int grid = (int)(blocks < 148 * 8 ? blocks : 148 * 8);
-  k_dft<<<grid, THREADS, smem, (cudaStream_t)stream>>>(reinterpret_cast<double2*>(data_complex), outer, n, inner,
+  k_dft<<<grid, THREADS, smem, (cudaStream_t)stream>>>(reinterpret_cast<double2*>(data_complex), outer, n, n1, inner,
                                                        inverse, reinterpret_cast<const double2*>(roots_complex));
   return done();
 }

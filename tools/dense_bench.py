@@ -49,7 +49,9 @@ def main():
     e1.record(st)
     torch.cuda.synchronize()
     dft_s = e0.elapsed_time(e1) / 1e3 / f.d
-    dft_flops = 8.0 * a.n * f.total            # complex MAC per output per input sample
+    n1 = next((q for q in range(2, int(a.n ** 0.5) + 1) if a.n % q == 0), 1)
+    macs = (n1 + a.n // n1 + 1) if n1 > 1 else a.n   # two-stage Cooley-Tukey in SMEM (csrc/dense.cu)
+    dft_flops = 8.0 * macs * f.total           # 8 flops per complex multiply-add
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     s0.record(st)
@@ -72,7 +74,8 @@ def main():
            "wall_ms_per_step": 1e3 * wall / a.steps, "launches_per_step": None,
            "hbm": {"bytes_per_step": bpp * f.total, "achieved_gbs": bpp * f.total * a.steps / dev / 1e9,
                    "peak_gbs": peaks["hbm_gbs"]},
-           "dft_kernel": {"ms_per_axis_pass": 1e3 * dft_s, "tflops": dft_flops / dft_s / 1e12,
+           "dft_kernel": {"ms_per_axis_pass": 1e3 * dft_s, "complex_macs_per_point": macs,
+                          "tflops": dft_flops / dft_s / 1e12,
                           "fp64_peak_tflops": fp64, "frac": dft_flops / dft_s / 1e12 / fp64}}
     if a.cpu and a.n <= 65:
         from oracle import dense as D
