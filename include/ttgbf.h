@@ -26,6 +26,7 @@
  *   ttgbf_greedy_cross        tt_algorithms.greedy_cross        tt_algorithms.py:463-596
  *                             (on the prior / likelihood / kernel black boxes)
  *   ttgbf_negative_mass       filters._negative_mass_tt         filters.py:427-436
+ *   ttgbf_filter_time_update_std  filters.tt_pmf_step time update (Algorithm 2) filters.py:855-885
  *   ttgbf_dense_*             filters.dense_fft_pmf_step pieces  filters.py:888-934
  *                             (the dense FFT PMF on the GPU)
  */
@@ -243,6 +244,16 @@ int ttgbf_filter_time_update(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgb
                              const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr, double* state,
                              int64_t state_cap, void* ws, int64_t ws_bytes, ttgbf_diag* diag,
                              void* stream);
+
+/* Algorithm 2 time update of tt_pmf_step (filters.py:876-885): transition
+ * cross over the 2d modes (io.pred = new grid, io.cur = old grid), backward
+ * contraction with the filtering TT in the state (tt_einsum_tpm,
+ * tt_algorithms.py:603-635), scale by the old cell volume, finalize.
+ * diag.cross[1] receives the transition cross info; d <= 8. */
+int ttgbf_filter_time_update_std(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
+                                 const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
+                                 ttgbf_tt* state_hdr, double* state, int64_t state_cap, void* ws, int64_t ws_bytes,
+                                 ttgbf_diag* diag, void* stream);
 
 /* ---- TT primitives (batched over `count` independent items, one CTA each).
  * Inputs/outputs are arrays of packed TTs: hdr[i] with data + i*cap. ---- */

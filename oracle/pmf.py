@@ -342,3 +342,36 @@ def step(axes, cores, spec, z, cfg, cc):
                       "filt_cores": fcores, "realign": rres.cores, "faxes": faxes,
                       "lik": diag.get("stage_lik"), "paxes": paxes}
     return paxes, out, diag
+
+
+# -- Algorithm 2: TT standard point-mass filter (filters.py:855-885) -------------
+
+def transition_values(spec, new_axes, old_axes, idx):
+    """transition_blackbox (filters.py:653-679) via _transition_values
+    (filters.py:580-588): N(x_new - F x_old; 0, Q) * cell_volume(old)."""
+    idx = np.asarray(idx)
+    d = len(new_axes)
+    xn = points_for(new_axes, idx[:, :d])
+    xo = points_for(old_axes, idx[:, d:])
+    F = np.asarray(spec["F"], dtype=float)
+    return Gauss(spec["Q"]).pdf(xn - xo @ F.T) * cell_volume(old_axes)
+
+
+def step_std(axes, cores, spec, z, cfg, cc):
+    """tt_pmf_step (filters.py:855-885): measurement update, moments, Kalman
+    prediction, new grid, transition cross over (new, old) modes, backward
+    contraction, scale by the old cell volume, finalize."""
+    diag = {"clipped_mass": 0.0, "outlier": False}
+    fcores = cores if z is None else measurement_update(axes, cores, spec, z, cfg, cc, diag)[0]
+    mean, cov, fixed = moments(axes, fcores)
+    diag["filt_mean"], diag["filt_cov"], diag["spd_fixed"] = mean, cov, fixed
+    pm, pc = kalman_predict(mean, cov, spec)
+    diag["pred_mean"], diag["pred_cov"] = pm, pc
+    new_axes = design_grid(pm, pc, cfg["n_per_axis"], cfg["sigma_mult"])
+    shape = tuple(a.size for a in new_axes) + tuple(a.size for a in axes)
+    tres = _cross(shape, lambda idx: transition_values(spec, new_axes, axes, idx), cc)
+    _record(diag, "transition", tres)
+    raw = T.scaled(T.einsum_tpm(tres.cores, fcores), cell_volume(axes))
+    out = finalize(raw, new_axes, cfg, diag)
+    diag["stages"] = {"transition": tres.cores, "filt_cores": fcores}
+    return new_axes, out, diag

@@ -221,3 +221,18 @@ def at_points(cores, axes, points) -> np.ndarray:
     out = acc[:, 0, 0]
     out[~alive] = 0.0
     return out
+
+
+def einsum_tpm(tcores, wcores):
+    """tt_einsum_tpm (tt_algorithms.py:603-635): contract the 2d-mode transition
+    TT with the d-mode weights over modes d..2d-1 by the backward fold
+    z <- einsum('anb,cnd,bd->ac'), then absorb z into core d-1."""
+    d = len(wcores)
+    if len(tcores) != 2 * d:
+        raise ValueError(f"transition tensor must have {2 * d} modes, got {len(tcores)}")
+    z = np.ones((1, 1))
+    for j in range(d - 1, -1, -1):
+        z = np.einsum("anb,cnd,bd->ac", tcores[d + j], wcores[j], z, optimize=True)
+    out = [np.asarray(c) for c in tcores[: d - 1]]
+    out.append(np.einsum("anb,bz->anz", tcores[d - 1], z))
+    return out

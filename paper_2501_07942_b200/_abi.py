@@ -81,6 +81,7 @@ SIGNATURES = {
     "ttgbf_filter_prior": [P, P, GridCfg, CrossCfg, P, I32, P, I32, P, P, I64, P, I64, P, P],
     "ttgbf_filter_measure": [P, GridCfg, CrossCfg, P, I32, P, I32, P, I32, P, P, I64, P, I64, P, P],
     "ttgbf_filter_time_update": [P, GridCfg, CrossCfg, P, I32, P, I32, P, I32, P, P, I64, P, I64, P, P],
+    "ttgbf_filter_time_update_std": [P, GridCfg, CrossCfg, P, I32, P, I32, P, P, I64, P, I64, P, P],
     "ttgbf_filter_run": [P, P, GridCfg, CrossCfg, RunCfg, P, P, P, I32, P, I32, P, I32, P, P, I64, P, I64, P, I32,
                          P, P, P],
     "ttgbf_tt_round": [P, P, I64, I32, F64, I32, P, P, I64, P, I64, P, P],

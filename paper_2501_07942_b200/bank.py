@@ -281,6 +281,27 @@ class FilterBank:
                 self.io["cur"][i] = payload[4].device()
         return dg
 
+    def time_update_std(self, geom):
+        """Algorithm 2 time update (tt_pmf_step, filters.py:876-885) onto the
+        predictive grid io.pred designed by geometry()."""
+        self._need_slot_per_filter()
+        act = np.zeros(self.count, dtype=np.int32)
+        for i, (st, _) in geom.items():
+            if st == "ok":
+                act[i] = 1
+        self.io["active"] = act
+        self._push_io()
+        self._launch("ttgbf_filter_time_update_std", self.lib.ttgbf_filter_time_update_std, self.model.ptr,
+                     self.gcfg, self.xcfg, self.io_dev.ptr, self.count, self.probes.ptr, len(self.probes_np),
+                     self.hdr.ptr, self.state.ptr, self.cfg.state_doubles, self.ws.ptr, self.cfg.ws_bytes,
+                     self.diag_dev.ptr, self.be.stream_ptr)
+        dg = self._diag()
+        for i, (st, payload) in geom.items():
+            if st == "ok" and dg["status"][i] == 0:
+                self.grids[i] = payload[4]
+                self.io["cur"][i] = payload[4].device()
+        return dg
+
     def step(self, z):
         """One tt_fft_pmf_step for every alive filter.
 

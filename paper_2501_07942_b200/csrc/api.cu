@@ -135,6 +135,26 @@ int ttgbf_filter_time_update(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgb
   return launch(nfilt, f, stream);
 }
 
+int ttgbf_filter_time_update_std(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
+                                 const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
+                                 ttgbf_tt* state_hdr, double* state, int64_t state_cap, void* ws, int64_t ws_bytes,
+                                 ttgbf_diag* diag, void* stream) {
+  auto f = LAMBDA(const Ctx& c0, int i, double* smem) {
+    if (!io[i].active) return;
+    Arena ar = make_arena(ws, ws_bytes, i);
+    ttgbf_diag* dg = diag + i;
+    Ctx c = c0;
+    c.prof = dg->prof;
+    int st = stage_time_std(c, ar, *model, gcfg, xcfg, io[i], probes, nprobes, state_hdr + i,
+                            state + (int64_t)i * state_cap, state_cap, dg, make_stage_smem(smem));
+    if (c.leader()) {
+      dg->status = st;
+      if ((int64_t)ar.peak > dg->ws_peak) dg->ws_peak = (int64_t)ar.peak;
+    }
+  };
+  return launch(nfilt, f, stream);
+}
+
 int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
                      ttgbf_run_cfg rcfg, ttgbf_filter_io* io, int32_t* kstep, const double* Z, int nfilt,
                      const int32_t* probes, int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr,

@@ -421,6 +421,60 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
 
 
 // ---------------------------------------------------------------------------
+// Algorithm 2 time update of tt_pmf_step (filters.py:876-885): transition
+// cross over the 2d modes (new grid io.pred, old grid io.cur), backward
+// contraction with the filtering TT, scale by the old cell volume, finalize
+// on the new grid.  The cross info lands in dg->cross[1] ("transition").
+// ---------------------------------------------------------------------------
+HDN int stage_time_std(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_grid_cfg& gcfg,
+                       const ttgbf_cross_cfg& xcfg, const ttgbf_filter_io& io, const int32_t* probes, int nprobes,
+                       ttgbf_tt* hdr, double* state, int64_t cap, ttgbf_diag* dg, StageSmem S) {
+  const int d = model.d;
+  if (2 * d > MAXD) return E_ARG;
+  double *ao[MAXD], *an[MAXD];
+  AxisGeom go[MAXD], gn[MAXD];
+  double so[MAXD], sn[MAXD];
+  CK(materialize_axes(c, ar, d, io.cur, ao, go, so));
+  CK(materialize_axes(c, ar, d, io.pred, an, gn, sn));
+  EvalSpec* sp;
+  CK(spec_alloc(c, ar, sp));
+  const double cv_old = cell_volume(so, d);
+  if (c.leader()) {
+    sp->kind = EV_TRANSITION;
+    sp->d = 2 * d;
+    sp->dhalf = d;
+    for (int k = 0; k < d; ++k) {
+      sp->n[k] = io.pred[k].n;
+      sp->axes[k] = an[k];
+      sp->n[d + k] = io.cur[k].n;
+      sp->axes[d + k] = ao[k];
+    }
+    for (int i = 0; i < MAXD * MAXD; ++i) { sp->F[i] = model.F[i]; sp->L[i] = model.Lq[i]; }
+    sp->log_norm = model.logn_q;
+    sp->cellvol = cv_old;
+  }
+  c.sync();
+  const TT filt = tt_view(hdr, state);
+  int64_t t0 = clk();
+  const size_t m0 = ar.mark();
+  TT tpm;
+  CrossInfo ci;
+  CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, nullptr, 0), S.xs, tpm, &ci, S.sm));
+  if (c.leader()) { put_cross(&dg->cross[1], ci); dg->cycles[4] += clk() - t0; }
+  CK(tt_compact(c, ar, m0, tpm));
+  t0 = clk();
+  const size_t m1 = ar.mark();
+  TT raw;
+  CK(tt_einsum_tpm(c, ar, tpm, filt, raw, S.sm));
+  CK(tt_compact(c, ar, m1, raw));
+  tt_scale(c, raw, cv_old);
+  CK(finalize_tt(c, ar, raw, gcfg, sn, probes, nprobes, dg, S.sm));
+  CK(tt_store(c, raw, hdr, state, cap));
+  if (c.leader()) { log_ranks(dg, 7, raw); dg->cycles[5] += clk() - t0; }
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
 // Persistent multi-step run: this filter's loop over rc.steps tt_fft_pmf_step
 // calls with device geometry, restarting from the prior after a failure or
 // at the end of its trajectory (bench / Monte Carlo driver).

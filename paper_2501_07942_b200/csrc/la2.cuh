@@ -589,6 +589,10 @@ HD void t_from_gram(const Ctx& c, const double* G, int jb, const double* tau, do
 // panel's T comes from one Gram GEMM of its explicit V (which the trailing
 // update needs anyway).
 constexpr int NS = 8;
+#ifndef TTGBF_QR2_MIN_ROWS
+#define TTGBF_QR2_MIN_ROWS 2048
+#endif
+constexpr int QR2_MIN_ROWS = TTGBF_QR2_MIN_ROWS;   // panels taller than this use two-level blocking
 HDN int geqrf_nb(const Ctx& c, Arena& ar, double* A, int64_t lda, int m, int n, double* tau, double* Ts,
                  double* sm) {
   const int k = imin(m, n);
@@ -597,7 +601,7 @@ HDN int geqrf_nb(const Ctx& c, Arena& ar, double* A, int64_t lda, int m, int n, 
     double* T = Ts + (int64_t)(j0 / NB) * NB * NB;
     const int64_t mr = m - j0;
     size_t mk = ar.mark();
-    if (mr <= 2048 || jb <= NS) {
+    if (mr <= QR2_MIN_ROWS || jb <= NS) {
       PROF(c, 16);
       qr_panel_nb(c, A, lda, m, j0, jb, tau, T, sm);
     } else {
@@ -616,12 +620,12 @@ HDN int geqrf_nb(const Ctx& c, Arena& ar, double* A, int64_t lda, int m, int n, 
       }
     }
     const bool trail = j0 + jb < n;
-    if (trail || !(mr <= 2048 || jb <= NS)) {
+    if (trail || !(mr <= QR2_MIN_ROWS || jb <= NS)) {
       PROF(c, 17);
       double *Vc, *G;
       ALLOC(Vc, double, mr * jb, ar);
       copy_v(c, A, lda, m, j0, jb, Vc);
-      if (!(mr <= 2048 || jb <= NS)) {
+      if (!(mr <= QR2_MIN_ROWS || jb <= NS)) {
         ALLOC(G, double, jb * jb, ar);
         // G = V^T V: A(i,p) = Vc[p + i*mr], B(p,j) = Vc[p + j*mr]
 #if ENGINE_DEVICE

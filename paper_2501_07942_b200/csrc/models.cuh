@@ -4,6 +4,8 @@
 //   EV_LIKELIHOOD p(z | x) with angle wrap                 models.py:72-82,146-153
 //   EV_KERNEL     N(disp F^T; 0, Q) * cell volume          filters.py:682-706
 //   EV_REALIGN    conv TT at F^{-1} y (multilinear)        filters.py:969-974
+//   EV_TRANSITION N(x_new - F x_old; 0, Q) * cell volume(old) over the
+//                 2d modes (new grid, old grid)           filters.py:580-588, 653-679
 // Gaussian densities follow models.py:30-69: value = exp(log_norm - |L^-1 r|^2/2)
 // with L the lower Cholesky factor (computed on the host by numpy).
 #pragma once
@@ -13,7 +15,7 @@
 
 namespace tg {
 
-enum EvalKind : int { EV_GAUSS = 0, EV_LIKELIHOOD = 1, EV_KERNEL = 2, EV_REALIGN = 3 };
+enum EvalKind : int { EV_GAUSS = 0, EV_LIKELIHOOD = 1, EV_KERNEL = 2, EV_REALIGN = 3, EV_TRANSITION = 4 };
 
 
 struct EvalSpec {
@@ -38,6 +40,8 @@ struct EvalSpec {
   double F[MAXD * MAXD];
   double steps[MAXD];
   double cellvol;
+  // transition (Algorithm 2): modes [0, dhalf) new grid, [dhalf, 2 dhalf) old grid
+  int dhalf;
   // realign
   double Finv[MAXD * MAXD];
   TT conv;
@@ -77,6 +81,17 @@ HD double eval_point(const EvalSpec& s, const int32_t* idx) {
         q[i] = acc;
       }
       return exp(s.log_norm - 0.5 * tri_quad(s.L, d, MAXD, q)) * s.cellvol;
+    }
+    case EV_TRANSITION: {
+      const int h = s.dhalf;
+      double xo[MAXD], diff[MAXD];
+      for (int k = 0; k < h; ++k) xo[k] = s.axes[h + k][idx[h + k]];
+      for (int i = 0; i < h; ++i) {   // x_new - (x_old @ F^T)
+        double acc = 0.0;
+        for (int j = 0; j < h; ++j) acc += xo[j] * s.F[i * MAXD + j];
+        diff[i] = s.axes[i][idx[i]] - acc;
+      }
+      return exp(s.log_norm - 0.5 * tri_quad(s.L, h, MAXD, diff)) * s.cellvol;
     }
     default:
       return NAN;

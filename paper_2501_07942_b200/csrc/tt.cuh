@@ -1322,6 +1322,61 @@ HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double to
 }
 
 // ---------------------------------------------------------------------------
+// tt_einsum_tpm (tt_algorithms.py:603-635): contract the 2d-mode transition TT
+// with the d-mode weights over modes d..2d-1.  Backward fold
+//   z(a, c) = sum_{n, b, e} T_{d+j}(a, n, b) W_j(c, n, e) z(b, e)
+// as two GEMMs per mode pair (M = W_j z^T, then T_{d+j} M^T), then core d-1
+// of the output = T_{d-1} x_3 z; cores 0..d-2 are T's.  Output in `out`.
+// ---------------------------------------------------------------------------
+HDN int tt_einsum_tpm(const Ctx& c, Arena& ar, const TT& T, const TT& W, TT& out, double* sm) {
+  const int d = W.d;
+  if (T.d != 2 * d) return E_ARG;
+  for (int k = 0; k < d; ++k)
+    if (T.n[d + k] != W.n[k]) return E_ARG;
+  int maxz = 1;
+  for (int k = 0; k <= T.d; ++k) maxz = imax(maxz, T.r[k]);
+  int maxw = 1;
+  for (int k = 0; k <= d; ++k) maxw = imax(maxw, W.r[k]);
+  int n[MAXD], r[MAXD + 1];
+  for (int k = 0; k < d; ++k) n[k] = T.n[k];
+  for (int k = 0; k < d; ++k) r[k] = T.r[k];
+  r[d] = W.r[0];   // = 1
+  CK(tt_alloc(ar, out, d, n, r));
+  const size_t mk = ar.mark();
+  double *z, *z2, *M;
+  int maxn = 1;
+  for (int k = 0; k < T.d; ++k) maxn = imax(maxn, T.n[k]);
+  ALLOC(z, double, (int64_t)maxz * maxw, ar);
+  ALLOC(z2, double, (int64_t)maxz * maxw, ar);
+  ALLOC(M, double, (int64_t)maxw * maxn * maxz, ar);
+  if (c.leader()) z[0] = 1.0;
+  c.sync();
+  int zb = 1, ze = 1;   // z is (zb x ze) row-major: rows = T right rank, cols = W right rank
+  for (int j = d - 1; j >= 0; --j) {
+    const double* Tc = T.c[d + j];
+    const double* Wc = W.c[j];
+    const int ta = T.r[d + j], tb = T.r[d + j + 1], wc = W.r[j], wd = W.r[j + 1], nn = W.n[j];
+    if (tb != zb || wd != ze) return E_ARG;
+    // M[(c, n), b] = sum_e W[(c, n), e] z[b, e]            ((wc*nn) x tb)
+    gemm(c, wc * nn, tb, wd, 1.0, Wc, wd, 1, z, 1, ze, 0.0, M, tb, 1, sm);
+    // z2[a, c] = sum_{(n, b)} T[a, (n, b)] M[(c, n), b]     (ta x wc)
+    gemm(c, ta, wc, nn * tb, 1.0, Tc, (int64_t)nn * tb, 1, M, 1, (int64_t)nn * tb, 0.0, z2, wc, 1, sm);
+    double* t = z; z = z2; z2 = t;
+    zb = ta;
+    ze = wc;
+  }
+  // cores 0..d-2 copied; core d-1: (r, n, zb) x z (zb x 1)
+  for (int k = 0; k + 1 < d; ++k) par_copy(c, out.c[k], T.c[k], T.size(k));
+  {
+    const int ra = T.r[d - 1], nn = T.n[d - 1];
+    gemm(c, ra * nn, ze, zb, 1.0, T.c[d - 1], zb, 1, z, ze, 1, 0.0, out.c[d - 1], ze, 1, sm);
+  }
+  c.sync();
+  ar.release(mk);
+  return OK;
+}
+
+// ---------------------------------------------------------------------------
 // Negative mass (filters.py:427-436): exact by full evaluation when the grid
 // has at most `guard` points, else the mean of max(-v,0) over the fixed
 // probe cells times the point count.  Returns the un-scaled sum or mean.

@@ -15,6 +15,7 @@ moments_from_pmd           filters.py:287-333 (TT branch)
 grid_redesign              filters.py:799-824 (TT branch)
 kalman_predict             filters.py:366-375
 tt_fft_pmf_step            filters.py:937-985
+tt_pmf_step                filters.py:855-885 (Algorithm 2)
 =========================  ===========================================
 
 Every density operation runs in ``libttgbf.so`` on the GPU; weights stay
@@ -40,7 +41,7 @@ from paper_2501_07942_b200.tensor_train import TensorTrain
 
 __all__ = ["CrossConfig", "DegenerateDensityError", "GridConfig", "PmdEstimate", "StepDiagnostics",
            "grid_redesign", "initial_pmd_tt", "kalman_predict", "measurement_update",
-           "moments_from_pmd", "tt_fft_pmf_step"]
+           "moments_from_pmd", "tt_fft_pmf_step", "tt_pmf_step"]
 
 
 class DegenerateDensityError(RuntimeError):
@@ -290,6 +291,47 @@ def tt_fft_pmf_step(pmd: PmdEstimate, model: StateSpaceModel, z, cfg: GridConfig
     diag.record_cross("realign", _cross_tuple(dt[0], 2))
     diag.mass_before_norm = float(dt["mass_before_norm"][0])
     diag.clipped_mass = float(dt["clipped_mass"][0])   # device accumulates over both stages
+    grid = Grid.from_axes(paxes)
+    w = _read(bank, grid)
+    diag.pmd_bytes = w.storage_bytes()
+    return PmdEstimate(grid, w, "predictive", diag)
+
+
+def tt_pmf_step(pmd: PmdEstimate, model: StateSpaceModel, z, cfg: GridConfig,
+                cross_cfg: CrossConfig) -> PmdEstimate:
+    """One Algorithm-2 step on the GPU (filters.py:855-885): measurement update,
+    moments, Kalman prediction, new grid, transition cross over the (new, old)
+    modes, tt_einsum_tpm contraction, scale by the old cell volume, finalize."""
+    if 2 * model.dim_x > _abi.MAXD:
+        raise ValueError("the transition tensor has 2d modes; d <= 8 on the device")
+    bank = _bank(model, cfg, cross_cfg)
+    _load(bank, pmd)
+    zz = np.zeros((1, model.dim_z)) if z is None else np.asarray(z, dtype=float)[None]
+    dm = bank.measure(zz, has_z=[0 if z is None else 1])
+    st = int(dm["status"][0])
+    if st != 0:
+        _raise(st, "tt_pmf_step (measurement)")
+    diag = StepDiagnostics()
+    if z is not None:
+        diag.record_cross("likelihood", _cross_tuple(dm[0], 0))
+        if dm["outlier"][0]:
+            diag.outlier = True
+            diag.warnings.append("measurement likelihood underflow; kept prior")
+    geom = bank.geometry(dm)
+    if geom[0][0] != "ok":
+        raise DegenerateDensityError("PMD has non-positive total mass")
+    mean, cov, fixed, _, paxes = geom[0][1]
+    diag.filt_moments = MomentEstimate(mean=mean, cov=cov)
+    diag.spd_fixed = fixed
+    pm, pc = geo.kalman_predict(mean, cov, model.F, model.Q)
+    diag.pred_moments = MomentEstimate(mean=pm, cov=pc)
+    dt = bank.time_update_std(geom)
+    st = int(dt["status"][0])
+    if st != 0:
+        _raise(st, "tt_pmf_step (time update)")
+    diag.record_cross("transition", _cross_tuple(dt[0], 1))
+    diag.mass_before_norm = float(dt["mass_before_norm"][0])
+    diag.clipped_mass = float(dt["clipped_mass"][0])
     grid = Grid.from_axes(paxes)
     w = _read(bank, grid)
     diag.pmd_bytes = w.storage_bytes()

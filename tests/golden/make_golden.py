@@ -181,6 +181,48 @@ def trajectories():
     np.savez_compressed(os.path.join(HERE, "trajectories.npz"), **out)
 
 
+def standard():
+    """tt_pmf_step trajectories (Algorithm 2) where the
+    transition cross converges: linear1d (the reference's own test config,
+    test_filters.py:307-321) and scaling2 with cross tol 1e-10."""
+    from paper_2501_07942_b200.configs import SPECS
+    lin1 = {"F": np.array([[0.9]]), "Q": np.array([[1.0]]), "R": np.array([[1.0]]), "h": "linear",
+            "H": np.array([[1.0]]), "angle_components": ()}
+    cases = [("linear1d", lin1, np.zeros(1), 2.0 * np.eye(1), {"tol": 1e-8, "max_rank": 20, "rng_seed": 0}, 5),
+             ("linear1d_exact", lin1, np.zeros(1), 2.0 * np.eye(1), {"tol": 1e-12, "max_rank": 40, "rng_seed": 0}, 5),
+             ("scaling2", SPECS["scaling2"], np.array([20.0, 20.0]), np.diag([9.0, 9.0]),
+              {"tol": 1e-10, "max_rank": 150, "rng_seed": 0}, 3)]
+    out = {}
+    for name, spec, mean, cov, cross, steps in cases:
+        m = ref_model(spec)
+        traj = rm.simulate(m, mean, cov, steps, seed=np.random.SeedSequence((2024, 0, 0)))
+        gcfg = rf.GridConfig(n_per_axis=33, sigma_mult=4.0, round_tol=1e-8)
+        ccfg = rta.CrossConfig(**cross)
+        t0 = time.time()
+        pmd = rf.initial_pmd_tt(MomentEstimate(mean, cov), gcfg, ccfg)
+        pack_tt(out, f"{name}/init", pmd.weights)
+        out[f"{name}/z"] = traj.measurements
+        done = 0
+        for k in range(steps):
+            try:
+                pmd = rf.tt_pmf_step(pmd, m, traj.measurements[k], gcfg, ccfg)
+            except rf.DegenerateDensityError:
+                break
+            dg = pmd.diag
+            out[f"{name}/{k}/filt_mean"] = dg.filt_moments.mean
+            out[f"{name}/{k}/filt_cov"] = dg.filt_moments.cov
+            out[f"{name}/{k}/axes"] = np.stack(pmd.grid.axes)
+            out[f"{name}/{k}/diag"] = np.array([dg.mass_before_norm, dg.clipped_mass, float(dg.outlier),
+                                                float(dg.spd_fixed)])
+            out[f"{name}/{k}/cross"] = np.array([list(dg.cross_info[c]) for c in ("likelihood", "transition")],
+                                                dtype=float)
+            pack_tt(out, f"{name}/{k}/pred", pmd.weights)
+            done += 1
+        out[f"{name}/done"] = np.array(done)
+        print(name, "steps", done, "%.1fs" % (time.time() - t0), flush=True)
+    np.savez_compressed(os.path.join(HERE, "standard.npz"), **out)
+
+
 def dense():
     """dense_fft_pmf_step trajectories: radar (d=2, full
     densities) and the BASELINE config-1 model (d=4, N=33; densities at 10^4
@@ -218,7 +260,7 @@ def dense():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["primitives", "crosses", "models", "trajectories", "dense"]
+    which = sys.argv[1:] or ["primitives", "crosses", "models", "trajectories", "dense", "standard"]
     for w in which:
         t = time.time()
         globals()[w]()
