@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--batch", type=int, default=2368)  # filters per GPU (8 per resident CTA slot)
+    p.add_argument("--batch", type=int, default=4096)  # filters per GPU (BASELINE config 5: 4096 trajectories)
     p.add_argument("--slots", type=int, default=0)     # resident CTAs (0: SMs x ttgbf_ctas_per_sm)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C5")
