@@ -277,22 +277,40 @@ __global__ void __launch_bounds__(THREADS) k_dft(double2* x, int64_t outer, int 
       m = n2;
       stride = n1;
     }
-    // final stage: X[k1 + n1 k2] = sum_j2 W_n2^(j2 k2) src[j2*n1 + k1]   (n1 = 1: direct DFT)
-    for (int e = threadIdx.x; e < n * LT; e += blockDim.x) {
-      const int om = e / LT, l = e % LT;
+    // final stage: X[k1 + n1 k2] = sum_j2 W_n2^(j2 k2) src[j2*n1 + k1]   (n1 = 1: direct DFT).
+    // A thread owns one line and KB consecutive k2 of one k1: each src value is
+    // loaded once for KB complex MACs, and the KB accumulators are independent.
+    constexpr int KB = 4;
+    const int kq = (m + KB - 1) / KB;
+    for (int e = threadIdx.x; e < stride * kq * LT; e += blockDim.x) {
+      const int l = e % LT, rest = e / LT;
+      const int k1 = rest % stride, k2b = (rest / stride) * KB;
       const int64_t L = l0 + l;
       if (L >= lines) continue;
-      const int k1 = om % stride, k2 = om / stride;
-      double re = 0.0, im = 0.0;
-      int q = 0;
-      const int dq = (k2 * stride) % n;
+      double re[KB], im[KB];
+      int q[KB], dq[KB];
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        re[u] = 0.0;
+        im[u] = 0.0;
+        q[u] = 0;
+        dq[u] = ((k2b + u) * stride) % n;
+      }
       for (int j2 = 0; j2 < m; ++j2) {
-        cmac(re, im, src[(j2 * stride + k1) * LT + l], rt[q]);
-        q += dq;
-        if (q >= n) q -= n;
+        const double2 a = src[(j2 * stride + k1) * LT + l];
+#pragma unroll
+        for (int u = 0; u < KB; ++u) {
+          cmac(re[u], im[u], a, rt[q[u]]);
+          q[u] += dq[u];
+          if (q[u] >= n) q[u] -= n;
+        }
       }
       const int64_t o = L / inner, i = L % inner;
-      x[(o * n + om) * inner + i] = make_double2(re * scale, im * scale);
+#pragma unroll
+      for (int u = 0; u < KB; ++u) {
+        const int k2 = k2b + u;
+        if (k2 < m) x[(o * n + k1 + stride * k2) * inner + i] = make_double2(re[u] * scale, im[u] * scale);
+      }
     }
   }
 }
