@@ -302,15 +302,16 @@ class FilterBank:
                 self.io["cur"][i] = payload[4].device()
         return dg
 
-    def step(self, z):
-        """One tt_fft_pmf_step for every alive filter.
+    def step(self, z, standard: bool = False):
+        """One tt_fft_pmf_step (standard=True: tt_pmf_step, Algorithm 2) for
+        every alive filter.
 
         Returns a dict with per-filter status (0 ok), filtering means/covs and
         the two diagnostic records.  Failed filters are marked dead.
         """
         dm = self.measure(z)
         geom = self.geometry(dm)
-        dt = self.time_update(geom)
+        dt = self.time_update_std(geom) if standard else self.time_update(geom)
         n = self.count
         status = np.full(n, -1, dtype=np.int64)
         means = np.full((n, self.d), np.nan)

@@ -36,7 +36,7 @@ import numpy as np
 from .bank import BankConfig, FilterBank
 from .configs import SPECS, scaling_spec, simulate
 
-FILTER_NAMES = ("ttfft-gpu",)
+FILTER_NAMES = ("ttfft-gpu", "tt-gpu", "fft-gpu")   # reference rows: ttfft, tt, fft
 COMPARE_SCENARIOS = ("radar", "linear1d", "linear2d")
 
 
@@ -169,9 +169,13 @@ def _pmd_bytes(bank: FilterBank) -> int:
 
 
 def run_filter_gpu(name, spec, mean, cov, states, meas, cfg: RunConfig, backend=None) -> FilterOutcome:
-    """_run_grid_filter (bench.py:317-392) for every run at once on the device."""
+    """_run_grid_filter (bench.py:317-392) for every run at once on the device
+    (ttfft-gpu: tt_fft_pmf_step; tt-gpu: tt_pmf_step), or run by run for the
+    dense fft-gpu filter (dense_fft_pmf_step)."""
     if name not in FILTER_NAMES:
         raise ConfigError(f"unknown filter {name!r}")
+    if name == "fft-gpu":
+        return _run_dense_gpu(name, spec, mean, cov, states, meas, cfg, backend)
     runs, k_f = meas.shape[0], meas.shape[1]
     d = np.asarray(spec["F"]).shape[0]
     bank = FilterBank(spec, cfg.bank_config(runs), runs, backend=backend)
@@ -189,7 +193,7 @@ def run_filter_gpu(name, spec, mean, cov, states, meas, cfg: RunConfig, backend=
         if sync:
             sync()
         t0 = time.perf_counter()
-        res = bank.step(meas[:, k])
+        res = bank.step(meas[:, k], standard=(name == "tt-gpu"))
         if sync:
             sync()
         times.append((time.perf_counter() - t0) / runs)
@@ -225,6 +229,42 @@ def run_filter_gpu(name, spec, mean, cov, states, meas, cfg: RunConfig, backend=
                          storage_estimated=False, ms_per_step=1000.0 * float(np.median(times)),
                          clipped_mass=clipped, max_mass_dev=mass_dev, failure=None, skipped=None,
                          diagnostics=diagnostics, trace=tuple(trace))
+
+
+def _run_dense_gpu(name, spec, mean, cov, states, meas, cfg: RunConfig, backend=None) -> FilterOutcome:
+    """The reference's dense 'fft' row (bench.py:321-327 with dense_fft_pmf_step)."""
+    from .dense import DegenerateDensityError, DenseFFTFilter
+    runs, k_f = meas.shape[0], meas.shape[1]
+    d = np.asarray(spec["F"]).shape[0]
+    f = DenseFFTFilter(spec, cfg.n_per_axis, cfg.sigma_mult, backend)
+    times, errors, trace = [], [], []
+    clipped = mass_dev = before_dev = 0.0
+    for r in range(runs):
+        f.initial(mean, cov)
+        for k in range(k_f):
+            f.be.sync()
+            t0 = time.perf_counter()
+            try:
+                dg = f.step(meas[r, k])
+            except DegenerateDensityError as exc:
+                return _failed(name, d, f"run {r} step {k}: {exc}")
+            f.be.sync()
+            times.append(time.perf_counter() - t0)
+            err = dg.filt_mean - states[r, k]
+            errors.append(err)
+            clipped = max(clipped, dg.clipped_mass)
+            if math.isfinite(dg.mass_before_norm):
+                before_dev = max(before_dev, abs(dg.mass_before_norm - 1.0))
+            pos, neg = f._reduce(f.w, f._axes_host(f.grid), 0)
+            mass_dev = max(mass_dev, abs((pos + neg) * f.grid.cell_volume() - 1.0))
+            if r == 0:
+                trace.append((float(k), *states[0, k], *dg.filt_mean, *err))
+    rmse = tuple(float(v) for v in np.sqrt(np.mean(np.square(np.array(errors)), axis=0)))
+    return FilterOutcome(name=name, dim=d, rmse=rmse, rel_diff_pct=None, bytes_tpm=f.total * 8,
+                         bytes_pmd=f.total * 8, storage_estimated=False,
+                         ms_per_step=1000.0 * float(np.median(times)), clipped_mass=clipped, max_mass_dev=mass_dev,
+                         failure=None, skipped=None,
+                         diagnostics=(("max_mass_before_norm_dev", before_dev),), trace=tuple(trace))
 
 
 def _tt_sum(cores) -> float:

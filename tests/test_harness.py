@@ -53,7 +53,7 @@ def _compare_with_oracle(backend, runs, k_f):
     1e-10 makes every cross exact (pivot-independent, SURVEY 8(c) tier 3);
     at the harness default 1e-2 single runs are ulp-chaotic."""
     from oracle import pmf
-    cfg = H.RunConfig(scenario="radar", runs=runs, k_f=k_f, cross_tol=1e-10)
+    cfg = H.RunConfig(scenario="radar", filters=("ttfft-gpu",), runs=runs, k_f=k_f, cross_tol=1e-10)
     rep = H.run_compare(cfg, backend=backend)
     row = rep.row("ttfft-gpu")
     assert row.failure is None, row.failure
@@ -89,3 +89,53 @@ def test_compare_radar_gpu_matches_oracle():
     if not torch.cuda.is_available():
         pytest.fail("GPU test run without a CUDA device")
     _compare_with_oracle(None, runs=4, k_f=4)
+
+
+def _compare_standard(backend):
+    """tt-gpu row (tt_pmf_step) on the linear1d scenario with an exact
+    transition cross, against the oracle run by run."""
+    from oracle import pmf
+    cfg = H.RunConfig(scenario="linear1d", filters=("tt-gpu",), runs=2, k_f=3, cross_tol=1e-12,
+                      cross_max_rank=40)
+    row = H.run_compare(cfg, backend=backend).row("tt-gpu")
+    assert row.failure is None, row.failure
+    spec, m, c = H.scenario_model("linear1d")
+    states, meas = H.trajectories(cfg, spec, m, c)
+    g = {"n_per_axis": 33, "sigma_mult": 4.0, "round_tol": 1e-8}
+    x = {"tol": 1e-12, "max_rank": 40, "rng_seed": 0}
+    errs = []
+    for r in range(cfg.runs):
+        axes, cores, _ = pmf.initial(m, c, g, x)
+        for k in range(cfg.k_f):
+            axes, cores, dg = pmf.step_std(axes, cores, spec, meas[r, k], g, x)
+            errs.append(dg["filt_mean"] - states[r, k])
+    rmse = np.sqrt(np.mean(np.square(np.array(errs)), axis=0))
+    assert np.allclose(row.rmse, rmse, rtol=1e-7, atol=0)
+
+
+def test_compare_standard_hostsim():
+    from hostsim import HostBackend
+    _compare_standard(HostBackend())
+
+
+@pytest.mark.gpu
+def test_compare_standard_and_dense_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+    _compare_standard(None)
+    from oracle import dense as D
+    cfg = H.RunConfig(scenario="radar", filters=("fft-gpu",), runs=2, k_f=3)
+    row = H.run_compare(cfg).row("fft-gpu")
+    assert row.failure is None, row.failure
+    spec, m, c = H.scenario_model("radar")
+    states, meas = H.trajectories(cfg, spec, m, c)
+    errs = []
+    for r in range(cfg.runs):
+        axes, w, _ = D.initial(m, c, {"n_per_axis": 33, "sigma_mult": 4.0})
+        for k in range(cfg.k_f):
+            axes, w, dg = D.step(axes, w, spec, meas[r, k], {"n_per_axis": 33, "sigma_mult": 4.0})
+            errs.append(dg["filt_mean"] - states[r, k])
+    rmse = np.sqrt(np.mean(np.square(np.array(errs)), axis=0))
+    assert np.allclose(row.rmse, rmse, rtol=1e-8, atol=0)
+    assert row.max_mass_dev <= 1e-12
