@@ -228,17 +228,37 @@ __device__ __forceinline__ void cmac(double& re, double& im, const double2 a, co
   im = fma(a.x, r.y, fma(a.y, r.x, im));
 }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
 __global__ void __launch_bounds__(THREADS) k_dft(double2* x, int64_t outer, int n, int n1, int64_t inner, int inverse,
-                                                 const double2* roots) {
+                                                 const double2* roots, int use_mma) {
   extern __shared__ double2 sh[];
   double2* xs = sh;               // [n][LT]
   double2* ys = sh + n * LT;      // [n][LT]  stage-1 output
   double2* rt = ys + n * LT;      // [n]
+  const int n2 = n / n1;
+  // DMMA final stage: the length-n2 DFT matrix W(k2, j2) = root[(j2 k2 n1) mod n]
+  // as real and imaginary planes, zero-padded to MP x KP (8 | MP, 4 | KP)
+  const int MP = (n2 + 7) & ~7, KP = (n2 + 3) & ~3;
+  double* wr = reinterpret_cast<double*>(rt + n);
+  double* wi = wr + MP * KP;
   for (int q = threadIdx.x; q < n; q += blockDim.x) {
     const double2 r = roots[q];
     rt[q] = inverse ? make_double2(r.x, -r.y) : r;
   }
-  const int n2 = n / n1;
+  if (use_mma) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < MP * KP; e += blockDim.x) {
+      const int k2 = e / KP, j2 = e % KP;
+      double2 w = make_double2(0.0, 0.0);
+      if (k2 < n2 && j2 < n2) w = rt[(int)(((int64_t)j2 * k2 * n1) % n)];
+      wr[e] = w.x;
+      wi[e] = w.y;
+    }
+  }
   const int64_t lines = outer * inner;
   const double scale = inverse ? 1.0 / (double)n : 1.0;
   for (int64_t l0 = (int64_t)blockIdx.x * LT; l0 < lines; l0 += (int64_t)gridDim.x * LT) {
@@ -276,6 +296,40 @@ __global__ void __launch_bounds__(THREADS) k_dft(double2* x, int64_t outer, int 
       src = ys;
       m = n2;
       stride = n1;
+    }
+    if (use_mma) {
+      // final stage on FP64 tensor cores: per k1, OUT (MP x LT) = W (MP x KP) SRC_k1 (KP x LT),
+      // complex as four real DMMA products.  Warp task = (k1, 8-row tile, 8-line tile).
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, ar = lane >> 2, ac = lane & 3;
+      const int tm_n = MP / 8, tasks = stride * tm_n * (LT / 8);
+      for (int t = warp; t < tasks; t += blockDim.x >> 5) {
+        const int tn = t % (LT / 8), tm = (t / (LT / 8)) % tm_n, k1 = t / (LT / 8 * tm_n);
+        double cr0 = 0.0, cr1 = 0.0, ci0 = 0.0, ci1 = 0.0;
+        const int row = tm * 8 + ar, col = tn * 8 + ar;
+        for (int k0 = 0; k0 < KP; k0 += 4) {
+          const int j2 = k0 + ac;
+          const double a_r = wr[row * KP + j2], a_i = wi[row * KP + j2];
+          const double2 b = j2 < m ? src[(j2 * stride + k1) * LT + col] : make_double2(0.0, 0.0);
+          dmma884(cr0, cr1, a_r, b.x);
+          dmma884(cr0, cr1, -a_i, b.y);
+          dmma884(ci0, ci1, a_r, b.y);
+          dmma884(ci0, ci1, a_i, b.x);
+        }
+        const int k2 = tm * 8 + ar;
+        if (k2 < m) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int l = tn * 8 + 2 * ac + h;
+            const int64_t L = l0 + l;
+            if (L < lines) {
+              const int64_t o = L / inner, i = L % inner;
+              x[(o * n + k1 + stride * k2) * inner + i] =
+                  make_double2((h ? cr1 : cr0) * scale, (h ? ci1 : ci0) * scale);
+            }
+          }
+        }
+      }
+      continue;
     }
     // final stage: X[k1 + n1 k2] = sum_j2 W_n2^(j2 k2) src[j2*n1 + k1]   (n1 = 1: direct DFT).
     // A thread owns one line and KB consecutive k2 of one k1: each src value is
@@ -421,7 +475,10 @@ int ttgbf_dense_dft(double* data_complex, const int32_t* shape, int d, int axis,
   int n1 = 1;                        // smallest prime factor (two-stage transform) or 1 (prime n)
   for (int p = 2; p * p <= n; ++p)
     if (n % p == 0) { n1 = p; break; }
-  const size_t smem = (size_t)(2 * n * LT + n) * sizeof(double2);
+  const int n2 = n / n1;
+  const int use_mma = (n1 > 1 && n2 <= 64) ? 1 : 0;   // tensor-core final stage for n2 <= 64
+  const int MP = (n2 + 7) & ~7, KP = (n2 + 3) & ~3;
+  const size_t smem = (size_t)(2 * n * LT + n) * sizeof(double2) + (use_mma ? (size_t)2 * MP * KP * sizeof(double) : 0);
   if (smem > 200 * 1024) return TTGBF_E_ARG;
   if (cudaFuncSetAttribute(k_dft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return TTGBF_E_CUDA;
@@ -429,7 +486,7 @@ int ttgbf_dense_dft(double* data_complex, const int32_t* shape, int d, int axis,
   const int64_t blocks = (lines + LT - 1) / LT;
   const int grid = (int)(blocks < 148 * 8 ? blocks : 148 * 8);
   k_dft<<<grid, THREADS, smem, (cudaStream_t)stream>>>(reinterpret_cast<double2*>(data_complex), outer, n, n1, inner,
-                                                       inverse, reinterpret_cast<const double2*>(roots_complex));
+                                                       inverse, reinterpret_cast<const double2*>(roots_complex), use_mma);
   return done();
 }
 
