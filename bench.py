@@ -51,8 +51,13 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C5")
     p.add_argument("--ws-mb", type=int, default=0)        # per resident CTA slot (0: split free HBM)
-    p.add_argument("--big-slots", type=int, default=40)   # overflow workspaces for oversized FFT products
-    p.add_argument("--big-mb", type=int, default=1280)
+    # overflow workspaces for oversized FFT products: 64 x 800 MB (products with
+    # 50 % headroom) + 24 x 1280 MB (the rest); measured: CTA time waiting for a
+    # buffer 800 -> 73 CTA-s per launch vs one class of 56 x 1280 MB
+    p.add_argument("--big-slots", type=int, default=64)
+    p.add_argument("--big-mb", type=int, default=800)
+    p.add_argument("--big2-slots", type=int, default=24)
+    p.add_argument("--big2-mb", type=int, default=1280)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-s", type=float, default=20.0)
     p.add_argument("--dump", default=None, help="save the timed run's step records (npz) for analysis")
@@ -226,13 +231,13 @@ def run_ours(args):
         args.slots = torch.cuda.get_device_properties(local).multi_processor_count * int(lib.ttgbf_ctas_per_sm())
     if args.ws_mb <= 0:
         free = torch.cuda.mem_get_info(local)[0]
-        reserve = (args.big_slots * args.big_mb << 20) + B * (1 << 17) * 8 + (8 << 30)
+        reserve = ((args.big_slots * args.big_mb + args.big2_slots * args.big2_mb) << 20) + B * (1 << 17) * 8 + (8 << 30)
         args.ws_mb = int(max(128, min(512, (free - reserve) // args.slots >> 20)))
     bcfg = BankConfig(n_per_axis=g["n_per_axis"], sigma_mult=g["sigma_mult"], round_tol=g["round_tol"],
                       round_max_rank=g["round_max_rank"], tol=x["tol"], max_rank=x["max_rank"],
                       rng_seed=x["rng_seed"], ws_bytes=args.ws_mb << 20, state_doubles=1 << 17,
                       cache_cap=1 << 20, ws_slots=args.slots, big_slots=args.big_slots,
-                      big_bytes=args.big_mb << 20)
+                      big_bytes=args.big_mb << 20, big2_slots=args.big2_slots, big2_bytes=args.big2_mb << 20)
     d = cfg["spec"]["F"].shape[0]
     b = np.atleast_2d(cfg["spec"]["R"]).shape[0]
     n = g["n_per_axis"]
@@ -362,7 +367,8 @@ def run_ours(args):
                        "share_rank_gt64": round(float(stats["prof"][29] / max(stats["cycles"].sum(), 1)), 4)},
         "completed_frac": stats["completed"] / max(1, B * args.steps),
         "ws_peak_mb": stats["ws_peak"] / 2 ** 20,
-        "overflow_ws": {"slots": args.big_slots, "mb": args.big_mb, "steps_used": stats["big_used"],
+        "overflow_ws": {"slots": args.big_slots, "mb": args.big_mb, "slots2": args.big2_slots, "mb2": args.big2_mb,
+                        "steps_used": stats["big_used"],
                         "peak_mb": stats["big_peak"] / 2 ** 20, "cta_seconds_waiting": stats["big_wait_s"]},
         "mean_cross_calls": stats["calls"],
         "step_gflop_p50_p90_p99_max": stats["step_gflop_pcts"],

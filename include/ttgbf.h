@@ -194,6 +194,14 @@ typedef struct {
   int64_t big_bytes;
   void* big_ws;
   int32_t* big_locks;
+  /* second, larger overflow class (nbig2 buffers of big2_bytes): a product
+   * that fits big_bytes tries the first class, then this one; a larger one
+   * waits for this class only.  nbig2 = 0: none. */
+  int32_t nbig2;
+  int32_t pad3;
+  int64_t big2_bytes;
+  void* big2_ws;
+  int32_t* big2_locks;
 } ttgbf_run_cfg;
 
 /* one record per filter per attempted step */

@@ -62,7 +62,9 @@ class RunCfg(ctypes.Structure):
     _fields_ = [("n_per_axis", ctypes.c_int32), ("kf", ctypes.c_int32), ("steps", ctypes.c_int32),
                 ("pad", ctypes.c_int32), ("sigma_mult", ctypes.c_double), ("prior_grid", Axis * MAXD),
                 ("nbig", ctypes.c_int32), ("pad2", ctypes.c_int32), ("big_bytes", ctypes.c_int64),
-                ("big_ws", ctypes.c_void_p), ("big_locks", ctypes.c_void_p)]
+                ("big_ws", ctypes.c_void_p), ("big_locks", ctypes.c_void_p),
+                ("nbig2", ctypes.c_int32), ("pad3", ctypes.c_int32), ("big2_bytes", ctypes.c_int64),
+                ("big2_ws", ctypes.c_void_p), ("big2_locks", ctypes.c_void_p)]
 
 
 class CrossCfg(ctypes.Structure):

@@ -54,6 +54,8 @@ class BankConfig:
     ws_slots: int = 0          # persistent run: workspace slots (0 = one per filter)
     big_slots: int = 0         # persistent run: overflow workspaces for oversized FFT products
     big_bytes: int = 3 << 29
+    big2_slots: int = 0        # second (larger) overflow class
+    big2_bytes: int = 3 << 30
 
     def grid_cfg(self):
         return _abi.GridCfg(self.round_tol, int(self.round_max_rank or 0),
@@ -166,6 +168,9 @@ class FilterBank:
         self.nbig = int(cfg.big_slots)
         self.big_ws = backend.empty(self.nbig * cfg.big_bytes) if self.nbig else None
         self.big_locks = backend.empty(4 * max(1, self.nbig))
+        self.nbig2 = int(cfg.big2_slots)
+        self.big2_ws = backend.empty(self.nbig2 * cfg.big2_bytes) if self.nbig2 else None
+        self.big2_locks = backend.empty(4 * max(1, self.nbig2))
         self.diag_dev = backend.empty(n * _abi.DIAG.itemsize)
         self.grids: list[geo.Axes | None] = [None] * n
         self.alive = np.zeros(n, dtype=bool)
@@ -361,6 +366,11 @@ class FilterBank:
         rc.big_bytes = int(self.cfg.big_bytes)
         rc.big_ws = self.big_ws.ptr if self.big_ws is not None else None
         rc.big_locks = self.big_locks.ptr
+        self.be.zero(self.big2_locks)
+        rc.nbig2 = self.nbig2
+        rc.big2_bytes = int(self.cfg.big2_bytes)
+        rc.big2_ws = self.big2_ws.ptr if self.big2_ws is not None else None
+        rc.big2_locks = self.big2_locks.ptr
         self.be.zero(self.diag_dev)
         zb = self.be.upload(Z)
         self.bytes_h2d += Z.nbytes

@@ -304,24 +304,36 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
 // FFT convolution + rounding inside a borrowed overflow workspace; the
 // rounded TT (small) is copied back into the slot arena at `mark`.
 HDN int conv_in_overflow(const Ctx& c, Arena& ar, size_t mark, const TT& ker, const TT& shifted,
-                         const ttgbf_grid_cfg& gcfg, const ttgbf_run_cfg& pool, ttgbf_diag* dg, TT& conv,
-                         double* sm) {
-  int bi = -1;
+                         const ttgbf_grid_cfg& gcfg, const ttgbf_run_cfg& pool, int64_t need, ttgbf_diag* dg,
+                         TT& conv, double* sm) {
+  // spin-acquire a buffer: the first class if the product fits it, else (or
+  // when all of those are busy) the second, larger class
+  // the first class takes a product only with 50 % headroom over the estimate
+  const bool small_ok = pool.nbig > 0 && need + need / 2 <= pool.big_bytes;
+  const bool large_ok = pool.nbig2 > 0 && need <= pool.big2_bytes;
+  const bool only_small = pool.nbig2 == 0;   // single class: any product that fits it
+  int bi = -1, cls = 0;
   if (c.leader()) {
 #if ENGINE_DEVICE
     const int64_t tw = clk();
     while (bi < 0) {
-      for (int i = 0; i < pool.nbig && bi < 0; ++i)
-        if (atomicCAS(&pool.big_locks[i], 0, 1) == 0) bi = i;
+      if (small_ok || only_small)
+        for (int i = 0; i < pool.nbig && bi < 0; ++i)
+          if (atomicCAS(&pool.big_locks[i], 0, 1) == 0) { bi = i; cls = 0; }
+      if (large_ok)
+        for (int i = 0; i < pool.nbig2 && bi < 0; ++i)
+          if (atomicCAS(&pool.big2_locks[i], 0, 1) == 0) { bi = i; cls = 1; }
       if (bi < 0) __nanosleep(4000);
     }
     dg->big_wait += clk() - tw;
 #else
     bi = 0;
+    cls = (small_ok || only_small) ? 0 : 1;
 #endif
   }
   bi = (int)bcast_i(c, bi);
-  Arena big = make_ws_arena(pool.big_ws, pool.big_bytes, bi);
+  cls = (int)bcast_i(c, cls);
+  Arena big = cls == 0 ? make_ws_arena(pool.big_ws, pool.big_bytes, bi) : make_ws_arena(pool.big2_ws, pool.big2_bytes, bi);
   TT big_conv;
   int st = tt_fft_conv(c, big, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, big_conv, sm);
   if (!st) {
@@ -337,7 +349,7 @@ HDN int conv_in_overflow(const Ctx& c, Arena& ar, size_t mark, const TT& ker, co
     if ((int64_t)big.peak > dg->big_peak) dg->big_peak = (int64_t)big.peak;
 #if ENGINE_DEVICE
     __threadfence();
-    atomicExch(&pool.big_locks[bi], 0);
+    atomicExch(cls == 0 ? &pool.big_locks[bi] : &pool.big2_locks[bi], 0);
 #endif
   }
   c.sync();
@@ -386,9 +398,11 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   for (int k = 0; k < d; ++k)
     pbytes += (int64_t)ker.r[k] * shifted.r[k] * ker.n[k] * ker.r[k + 1] * shifted.r[k + 1] * 8;
   const int64_t need = pbytes + pbytes / 16 + ((int64_t)64 << 20);   // + rounding temporaries
-  if (pool && pool->nbig > 0 && (int64_t)(ar.cap - ar.off) < need) {
-    if (need > pool->big_bytes) return E_WORKSPACE;
-    CK(conv_in_overflow(c, ar, m0, ker, shifted, gcfg, *pool, dg, conv, S.sm));
+  if (pool && (pool->nbig > 0 || pool->nbig2 > 0) && (int64_t)(ar.cap - ar.off) < need) {
+    const bool fits = (pool->nbig > 0 && need + need / 2 <= pool->big_bytes) ||
+                      (pool->nbig2 > 0 && need <= pool->big2_bytes) || (pool->nbig2 == 0 && need <= pool->big_bytes);
+    if (!fits) return E_WORKSPACE;
+    CK(conv_in_overflow(c, ar, m0, ker, shifted, gcfg, *pool, need, dg, conv, S.sm));
   } else {
     CK(tt_fft_conv(c, ar, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, conv, S.sm));
     CK(tt_compact(c, ar, m0, conv));
