@@ -370,7 +370,7 @@ extern "C" int ttgbf_test_draws(int kind, uint64_t* state6, const int* shape, in
     std::vector<uint8_t> flags(size + 16);
     std::vector<uint32_t> gset(4 * (size + 16) + 64);
     warp_choice(c, &g, &jt, pop, size, out, disp.data(), touch.data(), draws.data(), flags.data(),
-                reinterpret_cast<uint32_t*>(smem.data() + SMEM_RED + SMEM_XBLK), 16384, gset.data(), &db);
+                reinterpret_cast<uint32_t*>(smem.data() + SMEM_RED + SMEM_XBLK), 2 * SMEM_SCRATCH_DOUBLES, gset.data(), &db);
     for (int64_t q = 0; q < pop; ++q)
       if (disp[q] != -1) return 99;   // displacement map must be restored
   }

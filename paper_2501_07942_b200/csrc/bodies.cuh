@@ -6,9 +6,9 @@
 
 namespace tg {
 
-constexpr int SMEM_RED = 64 + 1024;       // reductions + scan buffer (doubles)
+constexpr int SMEM_RED = 64 + 320;        // reductions + block_reduce_vec partials (8 warps x 33)
 constexpr int SMEM_XBLK = 128;            // XShared + XState (doubles)
-constexpr int SMEM_SCRATCH = 8192;        // gemm tiles / QR / chain evaluation
+constexpr int SMEM_SCRATCH = SMEM_SCRATCH_DOUBLES;   // gemm tiles / QR / chain evaluation
 constexpr int SMEM_DOUBLES = SMEM_RED + SMEM_XBLK + SMEM_SCRATCH;
 constexpr int BLOCK_THREADS = 256;
 // resident CTAs per SM the kernels are built for (registers <= 64K / (256 *

@@ -198,7 +198,7 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
     Key* sk = mkeys;
     if (!presorted) {
       PROF(c, 0);
-      const bool in_smem = P * (int64_t)sizeof(Key) <= (int64_t)(8192 * sizeof(double));
+      const bool in_smem = P * (int64_t)sizeof(Key) <= (int64_t)(SMEM_SCRATCH_DOUBLES * sizeof(double));
       if (in_smem) {
         sk = reinterpret_cast<Key*>(sm);
       } else {

@@ -33,6 +33,9 @@
 namespace tg {
 
 constexpr int MAXD = 16;      // max number of modes (state dimension)
+// general SMEM scratch per CTA (doubles): sized so two CTAs need <= 100 KB of
+// shared memory and the SM keeps ~156 KB of L1 for the L2-streamed working set
+constexpr int SMEM_SCRATCH_DOUBLES = 5632;
 constexpr int MAXB = 16;      // max measurement dimension
 
 // status codes (mirrored in include/ttgbf.h)

@@ -326,8 +326,8 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
   ALLOC(e, double, X_SCAN, ar);
   {
     PROF(c, 10);
-    warp_choice(c, &sh->rng, rws.jt, g.nrow, qr, cr, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
-    warp_choice(c, &sh->rng, rws.jt, g.ncol, qc, cc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, g.nrow, qr, cr, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, g.ncol, qc, cc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
   }
   if (c.leader()) {
     for (int i = 0; i < qr; ++i)
@@ -364,7 +364,7 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
     int nsr = 0;
     if (g.nrow > X_SCAN) {
       PROF(c, 10);
-      warp_choice(c, &sh->rng, rws.jt, g.nrow, X_SCAN, br, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+      warp_choice(c, &sh->rng, rws.jt, g.nrow, X_SCAN, br, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
     }
     if (c.leader()) {
       if (g.nrow > X_SCAN) nsr = X_SCAN;
@@ -384,7 +384,7 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
     int nsc = 0;
     if (g.ncol > X_SCAN) {
       PROF(c, 10);
-      warp_choice(c, &sh->rng, rws.jt, g.ncol, X_SCAN, bc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+      warp_choice(c, &sh->rng, rws.jt, g.ncol, X_SCAN, bc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
     }
     if (c.leader()) {
       if (g.ncol > X_SCAN) nsc = X_SCAN;
@@ -446,7 +446,7 @@ HDN int x_check(const Ctx& c, Arena& ar, Cache* C, XShared* sh, const ChoiceWs& 
   ALLOC(tv, double, K, ar);
   if (cnt > count) {
     PROF(c, 10);
-    warp_choice(c, &sh->rng, rws.jt, cnt, count, sel, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 16384, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, cnt, count, sel, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
   } else if (c.leader()) {
     for (int64_t i = 0; i < cnt; ++i) sel[i] = i;
   }

@@ -355,13 +355,14 @@ __device__ __noinline__ void gemm_vtc_dev(const Ctx& c, int64_t mr, int jb, int 
 
 // C (mr x nc, col-major ld ldc) -= V (mr x jb, col-major ld ldv) W2 (jb x nc,
 // row-major ld nc), jb <= 4*KS.  W2 is staged in SMEM in column chunks of
-// 192 (ld 196: conflict-free B fragments); warps stream 8-row blocks of C
+// 160 (ld 164: conflict-free B fragments); warps stream 8-row blocks of C
 // and V straight from global memory, C fragments are loaded into the
 // accumulators, updated with -V fragments and stored back.
 template <int KS>
 __device__ __noinline__ void gemm_cmvw_dev(const Ctx& c, int64_t mr, int jb, int nc, const double* V, int64_t ldv,
                                            const double* W2, double* C, int64_t ldc, double* sm) {
-  constexpr int CH = 192, LDW = 196;
+  constexpr int CH = 160, LDW = 164;
+  static_assert(4 * KS * LDW <= SMEM_SCRATCH_DOUBLES, "W2 chunk exceeds the SMEM scratch");
   const int warp = c.tid >> 5, lane = c.tid & 31, ar = lane >> 2, ac = lane & 3;
   const int64_t nblk = (mr + 7) / 8;
   for (int n0 = 0; n0 < nc; n0 += CH) {
