@@ -272,6 +272,8 @@ def run_ours(args):
     stats["completed"] = int(ok.sum())
     stats["failed"] = int((recs["status"] > 0).sum())
     stats["restarts"] = int((recs["status"] != 0).sum())
+    vals, cnts = np.unique(recs["status"], return_counts=True)
+    stats["status_counts"] = {str(int(v)): int(n) for v, n in zip(vals, cnts)}
     step_fl = []
     for i, s_ in zip(*np.nonzero(recs["status"] >= 0)):
         fl = sum(rl.rec_flops(recs[i, s_], d, b, n))
@@ -343,7 +345,8 @@ def run_ours(args):
         "config": {"workload": WORKLOAD, "filters_per_gpu": B, "runs": world * B, "parallelism": f"dp{world}",
                    "workspace_slots": args.slots, "workspace_mb_per_slot": args.ws_mb,
                    "l2": "per-filter working sets stream from HBM (batch footprint >> 126 MB L2)",
-                   "completed_steps": done_all, "restarts": stats["restarts"], "failed_steps": stats["failed"]},
+                   "completed_steps": done_all, "restarts": stats["restarts"], "failed_steps": stats["failed"],
+                   "status_counts": stats["status_counts"]},
         "gpu_launches": len(bank.timeline),
         "launch_note": "one persistent ttgbf_filter_run launch runs all K steps of all filters (device geometry)",
         "roofline": {"bound": "tensor", "precision": "fp64", "kernel": dom, "achieved": achieved,

@@ -237,6 +237,54 @@ HDN int stage_prior(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttg
   return OK;
 }
 
+// Borrow an overflow buffer (spin-acquire): the first class if `need` fits it
+// with 50 % headroom, else (or when those are busy) the second, larger class.
+// Returns the arena over it; *cls / *bi identify it for overflow_release.
+HDN Arena overflow_acquire(const Ctx& c, const ttgbf_run_cfg& pool, int64_t need, ttgbf_diag* dg, int* cls_out,
+                           int* bi_out) {
+  const bool small_ok = pool.nbig > 0 && need + need / 2 <= pool.big_bytes;
+  const bool large_ok = pool.nbig2 > 0 && need <= pool.big2_bytes;
+  const bool only_small = pool.nbig2 == 0;
+  int bi = -1, cls = 0;
+  if (c.leader()) {
+#if ENGINE_DEVICE
+    const int64_t tw = clk();
+    while (bi < 0) {
+      if (small_ok || only_small)
+        for (int i = 0; i < pool.nbig && bi < 0; ++i)
+          if (atomicCAS(&pool.big_locks[i], 0, 1) == 0) { bi = i; cls = 0; }
+      if (large_ok)
+        for (int i = 0; i < pool.nbig2 && bi < 0; ++i)
+          if (atomicCAS(&pool.big2_locks[i], 0, 1) == 0) { bi = i; cls = 1; }
+      if (bi < 0) __nanosleep(4000);
+    }
+    dg->big_wait += clk() - tw;
+#else
+    bi = 0;
+    cls = (small_ok || only_small) ? 0 : 1;
+#endif
+  }
+  bi = (int)bcast_i(c, bi);
+  cls = (int)bcast_i(c, cls);
+  *cls_out = cls;
+  *bi_out = bi;
+  return cls == 0 ? make_ws_arena(pool.big_ws, pool.big_bytes, bi) : make_ws_arena(pool.big2_ws, pool.big2_bytes, bi);
+}
+
+HDN void overflow_release(const Ctx& c, const ttgbf_run_cfg& pool, const Arena& big, int cls, int bi,
+                          ttgbf_diag* dg) {
+  c.sync();
+  if (c.leader()) {
+    dg->big_used += 1;
+    if ((int64_t)big.peak > dg->big_peak) dg->big_peak = (int64_t)big.peak;
+#if ENGINE_DEVICE
+    __threadfence();
+    atomicExch(cls == 0 ? &pool.big_locks[bi] : &pool.big2_locks[bi], 0);
+#endif
+  }
+  c.sync();
+}
+
 // ---------------------------------------------------------------------------
 // measurement_update (TT branch, filters.py:521-563) + raw moments of the
 // filtering density (filters.py:297-322).  Outlier keeps the prior.
@@ -244,7 +292,7 @@ HDN int stage_prior(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttg
 HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgbf_grid_cfg& gcfg,
                              const ttgbf_cross_cfg& xcfg, const ttgbf_filter_io& io, const int32_t* probes,
                              int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* hdr, double* state,
-                             int64_t cap, ttgbf_diag* dg, StageSmem S) {
+                             int64_t cap, ttgbf_diag* dg, StageSmem S, const ttgbf_run_cfg* pool = nullptr) {
   const int d = model.d;
   double* axes[MAXD];
   AxisGeom geo[MAXD];
@@ -268,20 +316,42 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
     if (c.leader()) dg->cycles[0] += t1 - t0;
     t0 = t1;
     const size_t mk2 = ar.mark();
-    TT prod;
-    CK(tt_hadamard(c, ar, p, lik, prod));
-    double* ws;
-    ALLOC(ws, double, 4096 + 16, ar);
-    const double mass = tt_sum(c, prod, ws) * cell_volume(steps, d);
-    if (!isfinite(mass) || mass <= MASS_FLOOR) {
-      if (c.leader()) dg->outlier = 1;
-      c.sync();
-    } else {
-      CK(tt_compact(c, ar, mk2, prod));
-      CK(finalize_tt(c, ar, prod, gcfg, steps, probes, nprobes, dg, S.sm));
+    // Hadamard + finalize on arena A; the state is written only at the end,
+    // so a product that outgrows the slot is redone in an overflow buffer
+    auto had_fin = [&](Arena& A) -> int {
+      const size_t ma = A.mark();
+      TT prod;
+      CK(tt_hadamard(c, A, p, lik, prod));
+      double* ws;
+      ALLOC(ws, double, 4096 + 16, A);
+      const double mass = tt_sum(c, prod, ws) * cell_volume(steps, d);
+      if (!isfinite(mass) || mass <= MASS_FLOOR) {
+        if (c.leader()) dg->outlier = 1;
+        c.sync();
+        return OK;
+      }
+      CK(tt_compact(c, A, ma, prod));
+      CK(finalize_tt(c, A, prod, gcfg, steps, probes, nprobes, dg, S.sm));
       CK(tt_store(c, prod, hdr, state, cap));
-      p = tt_view(hdr, state);
+      return OK;
+    };
+    const double clipped0 = dg->clipped_mass;
+    int hst = had_fin(ar);
+    if (hst == E_WORKSPACE && pool && (pool->nbig > 0 || pool->nbig2 > 0)) {
+      ar.release(mk2);
+      if (c.leader()) dg->clipped_mass = clipped0;
+      c.sync();
+      int64_t pb = 0;
+      for (int k = 0; k < d; ++k) pb += (int64_t)p.r[k] * lik.r[k] * p.n[k] * p.r[k + 1] * lik.r[k + 1] * 8;
+      int64_t nd = pb + pb / 16 + ((int64_t)64 << 20);
+      if (nd < (int64_t)ar.cap) nd = (int64_t)ar.cap;
+      int cls, bi;
+      Arena big = overflow_acquire(c, *pool, nd, dg, &cls, &bi);
+      hst = had_fin(big);
+      overflow_release(c, *pool, big, cls, bi, dg);
     }
+    CK(hst);
+    p = tt_view(hdr, state);
   }
   if (c.leader()) { log_ranks(dg, 2, p); dg->cycles[1] += clk() - t0; }
   t0 = clk();
@@ -306,34 +376,8 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
 HDN int conv_in_overflow(const Ctx& c, Arena& ar, size_t mark, const TT& ker, const TT& shifted,
                          const ttgbf_grid_cfg& gcfg, const ttgbf_run_cfg& pool, int64_t need, ttgbf_diag* dg,
                          TT& conv, double* sm) {
-  // spin-acquire a buffer: the first class if the product fits it, else (or
-  // when all of those are busy) the second, larger class
-  // the first class takes a product only with 50 % headroom over the estimate
-  const bool small_ok = pool.nbig > 0 && need + need / 2 <= pool.big_bytes;
-  const bool large_ok = pool.nbig2 > 0 && need <= pool.big2_bytes;
-  const bool only_small = pool.nbig2 == 0;   // single class: any product that fits it
-  int bi = -1, cls = 0;
-  if (c.leader()) {
-#if ENGINE_DEVICE
-    const int64_t tw = clk();
-    while (bi < 0) {
-      if (small_ok || only_small)
-        for (int i = 0; i < pool.nbig && bi < 0; ++i)
-          if (atomicCAS(&pool.big_locks[i], 0, 1) == 0) { bi = i; cls = 0; }
-      if (large_ok)
-        for (int i = 0; i < pool.nbig2 && bi < 0; ++i)
-          if (atomicCAS(&pool.big2_locks[i], 0, 1) == 0) { bi = i; cls = 1; }
-      if (bi < 0) __nanosleep(4000);
-    }
-    dg->big_wait += clk() - tw;
-#else
-    bi = 0;
-    cls = (small_ok || only_small) ? 0 : 1;
-#endif
-  }
-  bi = (int)bcast_i(c, bi);
-  cls = (int)bcast_i(c, cls);
-  Arena big = cls == 0 ? make_ws_arena(pool.big_ws, pool.big_bytes, bi) : make_ws_arena(pool.big2_ws, pool.big2_bytes, bi);
+  int cls, bi;
+  Arena big = overflow_acquire(c, pool, need, dg, &cls, &bi);
   TT big_conv;
   int st = tt_fft_conv(c, big, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, big_conv, sm);
   if (!st) {
@@ -343,16 +387,7 @@ HDN int conv_in_overflow(const Ctx& c, Arena& ar, size_t mark, const TT& ker, co
       for (int k = 0; k < conv.d; ++k) par_copy(c, conv.c[k], big_conv.c[k], conv.size(k));
     }
   }
-  c.sync();
-  if (c.leader()) {
-    dg->big_used += 1;
-    if ((int64_t)big.peak > dg->big_peak) dg->big_peak = (int64_t)big.peak;
-#if ENGINE_DEVICE
-    __threadfence();
-    atomicExch(cls == 0 ? &pool.big_locks[bi] : &pool.big2_locks[bi], 0);
-#endif
-  }
-  c.sync();
+  overflow_release(c, pool, big, cls, bi, dg);
   return st;
 }
 
@@ -398,14 +433,30 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   for (int k = 0; k < d; ++k)
     pbytes += (int64_t)ker.r[k] * shifted.r[k] * ker.n[k] * ker.r[k + 1] * shifted.r[k + 1] * 8;
   const int64_t need = pbytes + pbytes / 16 + ((int64_t)64 << 20);   // + rounding temporaries
-  if (pool && (pool->nbig > 0 || pool->nbig2 > 0) && (int64_t)(ar.cap - ar.off) < need) {
-    const bool fits = (pool->nbig > 0 && need + need / 2 <= pool->big_bytes) ||
-                      (pool->nbig2 > 0 && need <= pool->big2_bytes) || (pool->nbig2 == 0 && need <= pool->big_bytes);
+  const bool have_pool = pool && (pool->nbig > 0 || pool->nbig2 > 0);
+  int cst = E_WORKSPACE;
+  int64_t nd = need;
+  if (!have_pool || (int64_t)(ar.cap - ar.off) >= need) {
+    // in the slot; if the rounding temporaries outgrow the estimate, the
+    // (deterministic) convolution is redone in an overflow buffer
+    const size_t mc = ar.mark();
+    cst = tt_fft_conv(c, ar, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, conv, S.sm);
+    if (cst == OK) {
+      CK(tt_compact(c, ar, m0, conv));
+    } else {
+      if (cst != E_WORKSPACE || !have_pool) return cst;
+      ar.release(mc);
+      if (nd < (int64_t)ar.cap) nd = (int64_t)ar.cap;
+    }
+  }
+  if (cst != OK) {
+    const bool fits = (pool->nbig > 0 && nd + nd / 2 <= pool->big_bytes) ||
+                      (pool->nbig2 > 0 && nd <= pool->big2_bytes) || (pool->nbig2 == 0 && nd <= pool->big_bytes);
     if (!fits) return E_WORKSPACE;
-    CK(conv_in_overflow(c, ar, m0, ker, shifted, gcfg, *pool, need, dg, conv, S.sm));
-  } else {
-    CK(tt_fft_conv(c, ar, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, conv, S.sm));
-    CK(tt_compact(c, ar, m0, conv));
+    cst = conv_in_overflow(c, ar, m0, ker, shifted, gcfg, *pool, nd, dg, conv, S.sm);
+    if (cst == E_WORKSPACE && pool->nbig2 > 0 && pool->big2_bytes > pool->big_bytes && nd + nd / 2 <= pool->big_bytes)
+      cst = conv_in_overflow(c, ar, m0, ker, shifted, gcfg, *pool, pool->big_bytes + 1, dg, conv, S.sm);   // large class
+    CK(cst);
   }
   if (c.leader()) { log_ranks(dg, 5, conv); dg->cycles[5] += clk() - t0; }
   t0 = clk();
@@ -535,7 +586,7 @@ HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
       for (int k = 0; k <= TTGBF_MAXD; ++k) dg->ranks[sl][k] = 0;
   }
   c.sync();
-  int st = stage_measure(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S);
+  int st = stage_measure(c, ar, model, gcfg, xcfg, *io, probes, nprobes, seeds, nseeds, hdr, state, cap, dg, S, &rc);
   ar.release(m0);
   if (!st) {
     int gst = 0;
