@@ -26,6 +26,9 @@
  *   ttgbf_greedy_cross        tt_algorithms.greedy_cross        tt_algorithms.py:463-596
  *                             (on the prior / likelihood / kernel black boxes)
  *   ttgbf_negative_mass       filters._negative_mass_tt         filters.py:427-436
+ *   ttgbf_eval_blackbox       the cross black boxes: prior pdf, likelihood,
+ *                             FFT kernel, realign evaluator     filters.py:504,697-729,969-979;
+ *                                                               models.py:150-153
  *   ttgbf_filter_time_update_std  filters.tt_pmf_step time update (Algorithm 2) filters.py:855-885
  *   ttgbf_dense_*             filters.dense_fft_pmf_step pieces  filters.py:888-934
  *                             (the dense FFT PMF on the GPU)
@@ -52,6 +55,7 @@ extern "C" {
 #define TTGBF_E_CUDA 6         /* CUDA launch / runtime error                   */
 #define TTGBF_E_LINALG 7       /* numpy.linalg.LinAlgError (singular F)         */
 #define TTGBF_E_DENSE_GUARD 8  /* DenseGuardError                                */
+#define TTGBF_E_STATE_CAP 9    /* output TT larger than the per-filter state slab */
 
 /* Equidistant axis: coordinate i = base + step * (i - off), evaluated with a
  * separate multiply and add (no FMA) so it equals numpy's construction in
@@ -204,14 +208,17 @@ typedef struct {
   int32_t* big2_locks;
 } ttgbf_run_cfg;
 
-/* one record per filter per attempted step */
+#define TTGBF_NCOV (TTGBF_MAXD * (TTGBF_MAXD + 1) / 2)
+
+/* one record per filter per attempted step; cov = filtered covariance, upper
+ * triangle packed row-major (i <= j), d*(d+1)/2 entries used */
 typedef struct {
   int32_t status;         /* 0 = step completed, else TTGBF_E_*; -1 = prior init failed */
   int32_t k;              /* trajectory index of the measurement used */
   int32_t spd_fixed;
   int32_t outlier;
   double mean[TTGBF_MAXD];
-  double cov_diag[TTGBF_MAXD];
+  double cov[TTGBF_NCOV];
   double mass_before_norm;
   double clipped_mass;
   int64_t calls[3];
@@ -303,11 +310,28 @@ int ttgbf_tt_sum_moments(const ttgbf_tt* hdr, const double* data, int64_t cap, i
 #define TTGBF_BB_GAUSS 0       /* prior pdf on the grid (uses prior)           */
 #define TTGBF_BB_LIKELIHOOD 1  /* p(z|x) on the grid (uses model, io.z)        */
 #define TTGBF_BB_KERNEL 2      /* FFT kernel on the grid (uses model)          */
+#define TTGBF_BB_REALIGN 3     /* conv TT (grid io.filt) at F^-1 y, y on io.pred */
 
 int ttgbf_greedy_cross(int kind, const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_cross_cfg xcfg,
                        const ttgbf_filter_io* io, int count, const int32_t* seeds, int nseeds,
                        ttgbf_tt* out_hdr, double* out, int64_t out_cap, void* ws, int64_t ws_bytes,
                        ttgbf_diag* diag, void* stream);
+
+/* The black boxes themselves at integer grid indices, without cross or cache
+ * (the values greedy_cross samples).  Replaces, per kind:
+ *   TTGBF_BB_GAUSS       initial_pmd_tt's eval_many           filters.py:504-505
+ *                        (GaussianDensity.pdf, models.py:60-66)
+ *   TTGBF_BB_LIKELIHOOD  StateSpaceModel.likelihood           models.py:150-153
+ *                        (measure :146-148, angle_wrap_residual :72-82)
+ *   TTGBF_BB_KERNEL      _kernel_values / fft_kernel_blackbox filters.py:697-729
+ *   TTGBF_BB_REALIGN     the realign evaluator                filters.py:969-979
+ *                        (tt_eval_at_points, tt_algorithms.py:721-745)
+ * Item i uses io[i] (cur grid and z; filt/pred grids for REALIGN), the TT
+ * tt_hdr[i] / tt + i*tt_cap (REALIGN only, may be NULL otherwise), idx + i*K*d
+ * (int32, K x d) and writes out + i*K; status[i] receives the item status. */
+int ttgbf_eval_blackbox(int kind, const ttgbf_model* model, const ttgbf_gauss* prior, const ttgbf_filter_io* io,
+                        const ttgbf_tt* tt_hdr, const double* tt, int64_t tt_cap, int count, const int32_t* idx,
+                        int64_t K, double* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream);
 
 /* negative mass of a normalised TT on grid `axes` (returned already
  * multiplied by the cell volume) */
@@ -321,6 +345,9 @@ int ttgbf_block_threads(void);
 int64_t ttgbf_smem_bytes(void);
 int ttgbf_ctas_per_sm(void);   /* resident CTAs per SM the kernels are built for */
 const char* ttgbf_status_string(int status);
+/* sizeof of the ABI structs, for binding checks: 0 axis, 1 tt, 2 cross_cfg,
+ * 3 grid_cfg, 4 diag, 5 model, 6 gauss, 7 filter_io, 8 run_cfg, 9 step_rec */
+int64_t ttgbf_sizeof(int which);
 
 /* ---- dense grid filter: dense_fft_pmf_step (filters.py:888-934) --------
  * Weights are C-order float64 arrays over the grid `axes` (d <= 8 axes);

@@ -24,6 +24,7 @@ STATUS = {
     8: "dense guard exceeded",
 }
 E_ARG, E_NONFINITE, E_DEGENERATE, E_WORKSPACE, E_CACHE = 1, 2, 3, 4, 5
+E_STATE_CAP = 9
 
 AXIS = np.dtype([("base", "f8"), ("step", "f8"), ("off", "i4"), ("n", "i4")], align=True)
 TT = np.dtype([("d", "i4"), ("n", "i4", MAXD), ("r", "i4", MAXD + 1), ("pad", "i4"),
@@ -42,8 +43,20 @@ MODEL = np.dtype([("d", "i4"), ("b", "i4"), ("hkind", "i4"), ("nang", "i4"), ("a
 GAUSS = np.dtype([("mean", "f8", MAXD), ("L", "f8", MAXD * MAXD), ("logn", "f8")], align=True)
 RUN_CFG_FIELDS = None
 STEP_REC = np.dtype([("status", "i4"), ("k", "i4"), ("spd_fixed", "i4"), ("outlier", "i4"), ("mean", "f8", MAXD),
-                     ("cov_diag", "f8", MAXD), ("mass_before_norm", "f8"), ("clipped_mass", "f8"),
+                     ("cov", "f8", MAXD * (MAXD + 1) // 2), ("mass_before_norm", "f8"), ("clipped_mass", "f8"),
                      ("calls", "i8", 3), ("ranks", "i4", (8, MAXD + 1)), ("cycles", "i8")], align=True)
+
+
+def rec_cov(rec, d: int) -> np.ndarray:
+    """Unpack STEP_REC covariances (upper triangle, row-major) to (..., d, d)."""
+    packed = np.asarray(rec["cov"])
+    out = np.zeros(packed.shape[:-1] + (d, d))
+    iu = np.triu_indices(d)
+    out[(...,) + iu] = packed[..., : len(iu[0])]
+    out[(...,) + (iu[1], iu[0])] = packed[..., : len(iu[0])]
+    return out
+
+
 FILTER_IO = np.dtype([("cur", AXIS, MAXD), ("filt", AXIS, MAXD), ("pred", AXIS, MAXD),
                       ("z", "f8", MAXB), ("has_z", "i4"), ("active", "i4")], align=True)
 
@@ -95,6 +108,8 @@ SIGNATURES = {
     "ttgbf_tt_sum_moments": [P, P, I64, I32, P, P, P, I64, P, P],
     "ttgbf_greedy_cross": [I32, P, P, CrossCfg, P, I32, P, I32, P, P, I64, P, I64, P, P],
     "ttgbf_negative_mass": [P, P, I64, I32, P, I64, P, I32, P, P, I64, P, P],
+    "ttgbf_eval_blackbox": [I32, P, P, P, P, P, I64, I32, P, I64, P, P, I64, P, P],
+    "ttgbf_sizeof": [I32],
     "ttgbf_version": [],
     "ttgbf_block_threads": [],
     "ttgbf_smem_bytes": [],
@@ -113,7 +128,16 @@ SIGNATURES = {
     "ttgbf_dense_real": [P, P, I64, P],
 }
 DENSE = frozenset(n for n in SIGNATURES if n.startswith("ttgbf_dense_"))
-RESTYPES = {"ttgbf_smem_bytes": I64, "ttgbf_status_string": ctypes.c_char_p}
+RESTYPES = {"ttgbf_smem_bytes": I64, "ttgbf_status_string": ctypes.c_char_p, "ttgbf_sizeof": I64}
+
+BB_GAUSS, BB_LIKELIHOOD, BB_KERNEL, BB_REALIGN = 0, 1, 2, 3
+
+
+def struct_sizes() -> dict:
+    """numpy / ctypes mirrors of the ABI structs, indexed like ttgbf_sizeof()."""
+    return {0: AXIS.itemsize, 1: TT.itemsize, 2: ctypes.sizeof(CrossCfg), 3: ctypes.sizeof(GridCfg),
+            4: DIAG.itemsize, 5: MODEL.itemsize, 6: GAUSS.itemsize, 7: FILTER_IO.itemsize,
+            8: ctypes.sizeof(RunCfg), 9: STEP_REC.itemsize}
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "_lib")

@@ -70,6 +70,7 @@ const char* ttgbf_status_string(int s) {
     case TTGBF_E_CUDA: return "CUDA error";
     case TTGBF_E_LINALG: return "singular matrix";
     case TTGBF_E_DENSE_GUARD: return "dense guard exceeded";
+    case TTGBF_E_STATE_CAP: return "TT larger than the per-filter state slab";
     default: return "unknown status";
   }
 }
@@ -342,6 +343,39 @@ int ttgbf_negative_mass(const ttgbf_tt* hdr, const double* data, int64_t cap, in
     if (c.leader()) status[i] = st;
   };
   return launch(count, f, stream);
+}
+
+int ttgbf_eval_blackbox(int kind, const ttgbf_model* model, const ttgbf_gauss* prior, const ttgbf_filter_io* io,
+                        const ttgbf_tt* tt_hdr, const double* tt, int64_t tt_cap, int count, const int32_t* idx,
+                        int64_t K, double* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream) {
+  if (kind < TTGBF_BB_GAUSS || kind > TTGBF_BB_REALIGN) return TTGBF_E_ARG;
+  if (kind == TTGBF_BB_GAUSS && prior == nullptr) return TTGBF_E_ARG;
+  if (kind == TTGBF_BB_REALIGN && (tt_hdr == nullptr || tt == nullptr)) return TTGBF_E_ARG;
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    Arena ar = make_arena(ws, ws_bytes, i);
+    const int d = model->d;
+    int st = body_eval_bb(c, ar, kind, *model, prior, io[i], tt_hdr ? tt_hdr + i : nullptr,
+                          tt ? tt + (int64_t)i * tt_cap : nullptr, idx + (int64_t)i * K * d, K,
+                          out + (int64_t)i * K, make_stage_smem(smem).sm);
+    if (c.leader()) status[i] = st;
+  };
+  return launch(count, f, stream);
+}
+
+int64_t ttgbf_sizeof(int which) {
+  switch (which) {
+    case 0: return (int64_t)sizeof(ttgbf_axis);
+    case 1: return (int64_t)sizeof(ttgbf_tt);
+    case 2: return (int64_t)sizeof(ttgbf_cross_cfg);
+    case 3: return (int64_t)sizeof(ttgbf_grid_cfg);
+    case 4: return (int64_t)sizeof(ttgbf_diag);
+    case 5: return (int64_t)sizeof(ttgbf_model);
+    case 6: return (int64_t)sizeof(ttgbf_gauss);
+    case 7: return (int64_t)sizeof(ttgbf_filter_io);
+    case 8: return (int64_t)sizeof(ttgbf_run_cfg);
+    case 9: return (int64_t)sizeof(ttgbf_step_rec);
+    default: return -1;
+  }
 }
 
 }  // extern "C"

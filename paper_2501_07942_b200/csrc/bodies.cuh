@@ -11,6 +11,7 @@ constexpr int SMEM_XBLK = 128;            // XShared + XState (doubles)
 constexpr int SMEM_SCRATCH = SMEM_SCRATCH_DOUBLES;   // gemm tiles / QR / chain evaluation
 constexpr int SMEM_DOUBLES = SMEM_RED + SMEM_XBLK + SMEM_SCRATCH;
 constexpr int BLOCK_THREADS = 256;
+static_assert(BLOCK_THREADS == 32 * CTA_WARPS, "CHAIN_MAXR assumes CTA_WARPS warps per CTA");
 // resident CTAs per SM the kernels are built for (registers <= 64K / (256 *
 // this), SMEM_DOUBLES * 8 + 1 KiB <= 228 KiB / this)
 #ifndef TTGBF_CTAS_PER_SM
@@ -96,7 +97,7 @@ HDN int body_eval_many(const Ctx& c, Arena& ar, const ttgbf_tt* h, const double*
   TT t = tt_view(h, const_cast<double*>(data));
   int maxr = 1;
   for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
-  if (maxr > 512) return E_ARG;
+  if (maxr > CHAIN_MAXR) return E_ARG;
   IndexSlice is{&t, idx, 0};
   return tt_eval_bucketed(c, ar, t, K, is, out, sm);
 }
@@ -107,7 +108,7 @@ HDN int body_eval_points(const Ctx& c, Arena& ar, const ttgbf_tt* h, const doubl
   TT t = tt_view(h, const_cast<double*>(data));
   int maxr = 1;
   for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
-  if (maxr > 512) return E_ARG;
+  if (maxr > CHAIN_MAXR) return E_ARG;
   double* ax[MAXD];
   AxisGeom geo[MAXD];
   double st[MAXD];
@@ -165,6 +166,58 @@ HDN int body_cross(const Ctx& c, Arena& ar, int kind, const ttgbf_model& model, 
   if (c.leader()) put_cross(&dg->cross[0], ci);
   c.sync();
   return tt_store(c, t, oh, out, ocap);
+}
+
+// Black-box evaluators at integer indices (no cross, no cache): the values
+// greedy_cross sees.  kind TTGBF_BB_GAUSS / _LIKELIHOOD / _KERNEL on io.cur,
+// TTGBF_BB_REALIGN: the TT (th, data) on grid io.filt at F^-1 y, y the io.pred
+// node of each index (filters.py:969-979).
+HDN int body_eval_bb(const Ctx& c, Arena& ar, int kind, const ttgbf_model& model, const ttgbf_gauss* prior,
+                     const ttgbf_filter_io& io, const ttgbf_tt* th, const double* data, const int32_t* idx,
+                     int64_t K, double* out, double* sm) {
+  const int d = model.d;
+  if (d < 1 || d > MAXD || K < 0) return E_ARG;
+  double* axes[MAXD];
+  AxisGeom geo[MAXD];
+  double steps[MAXD];
+  CK(materialize_axes(c, ar, d, kind == TTGBF_BB_REALIGN ? io.pred : io.cur, axes, geo, steps));
+  EvalSpec* sp;
+  CK(spec_alloc(c, ar, sp));
+  if (kind == TTGBF_BB_REALIGN) {
+    if (th == nullptr || th->d != d) return E_ARG;
+    const TT t = tt_view(th, const_cast<double*>(data));
+    int maxr = 1;
+    for (int k = 0; k <= d; ++k) maxr = imax(maxr, t.r[k]);
+    if (maxr > CHAIN_MAXR) return E_ARG;
+    double* fax[MAXD];
+    AxisGeom fgeo[MAXD];
+    double fsteps[MAXD];
+    CK(materialize_axes(c, ar, d, io.filt, fax, fgeo, fsteps));
+    if (c.leader()) {
+      spec_grid(*sp, d, axes, io.pred);
+      sp->kind = EV_REALIGN;
+      for (int i = 0; i < MAXD * MAXD; ++i) sp->Finv[i] = model.Finv[i];
+      sp->conv = t;
+      for (int k = 0; k < d; ++k) sp->geo[k] = fgeo[k];
+    }
+    c.sync();
+    double* coords;
+    ALLOC(coords, double, K * d, ar);
+    for (int64_t e = c.tid; e < K * d; e += c.nt) coords[e] = realign_coord(*sp, idx + (e / d) * d, (int)(e % d));
+    c.sync();
+    PointSlice<PtsFn> ps{&sp->conv, sp->geo, PtsFn{coords, d}, 0, 0.0};
+    return tt_eval_bucketed(c, ar, sp->conv, K, ps, out, sm);
+  }
+  if (c.leader()) {
+    spec_grid(*sp, d, axes, io.cur);
+    if (kind == TTGBF_BB_GAUSS) spec_prior(*sp, *prior);
+    else if (kind == TTGBF_BB_LIKELIHOOD) spec_likelihood(*sp, model, io.z);
+    else spec_kernel(*sp, model, steps);
+  }
+  c.sync();
+  for (int64_t j = c.tid; j < K; j += c.nt) out[j] = eval_point(*sp, idx + j * d);
+  c.sync();
+  return OK;
 }
 
 }  // namespace tg

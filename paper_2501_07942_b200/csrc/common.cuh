@@ -36,6 +36,9 @@ constexpr int MAXD = 16;      // max number of modes (state dimension)
 // general SMEM scratch per CTA (doubles): sized so two CTAs need <= 100 KB of
 // shared memory and the SM keeps ~156 KB of L1 for the L2-streamed working set
 constexpr int SMEM_SCRATCH_DOUBLES = 5632;
+constexpr int CTA_WARPS = 8;  // BLOCK_THREADS / 32
+// widest TT rank tt_chain_eval can hold: two rank vectors per warp in the scratch
+constexpr int CHAIN_MAXR = SMEM_SCRATCH_DOUBLES / (2 * CTA_WARPS);
 constexpr int MAXB = 16;      // max measurement dimension
 
 // status codes (mirrored in include/ttgbf.h)
@@ -49,6 +52,7 @@ enum Status : int {
   E_CUDA = 6,
   E_LINALG = 7,       // singular dynamics (numpy.linalg.LinAlgError)
   E_DENSE_GUARD = 8,  // DenseGuardError
+  E_STATE_CAP = 9,    // output TT larger than the state slab (not an arena failure)
 };
 
 #define CK(expr) do { int _st = (expr); if (_st) return _st; } while (0)

@@ -62,7 +62,7 @@ HD double cell_volume(const double* steps, int d) {
 HDN int tt_store(const Ctx& c, const TT& t, ttgbf_tt* hdr, double* data, int64_t cap) {
   int64_t need = 0;
   for (int k = 0; k < t.d; ++k) need += t.size(k);
-  if (need > cap) return E_WORKSPACE;
+  if (need > cap) return E_STATE_CAP;
   int64_t off = 0;
   for (int k = 0; k < t.d; ++k) {
     par_copy(c, data + off, t.c[k], t.size(k));
@@ -239,9 +239,17 @@ HDN int stage_prior(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttg
 
 // Borrow an overflow buffer (spin-acquire): the first class if `need` fits it
 // with 50 % headroom, else (or when those are busy) the second, larger class.
-// Returns the arena over it; *cls / *bi identify it for overflow_release.
-HDN Arena overflow_acquire(const Ctx& c, const ttgbf_run_cfg& pool, int64_t need, ttgbf_diag* dg, int* cls_out,
-                           int* bi_out) {
+// Returns E_WORKSPACE at once when no class can ever hold `need` (instead of
+// spinning forever); otherwise *big is the arena over the buffer and *cls /
+// *bi identify it for overflow_release.
+HD bool overflow_fits(const ttgbf_run_cfg& pool, int64_t need) {
+  return (pool.nbig > 0 && need + need / 2 <= pool.big_bytes) || (pool.nbig2 > 0 && need <= pool.big2_bytes) ||
+         (pool.nbig2 == 0 && pool.nbig > 0 && need <= pool.big_bytes);
+}
+
+HDN int overflow_acquire(const Ctx& c, const ttgbf_run_cfg& pool, int64_t need, ttgbf_diag* dg, Arena* big,
+                         int* cls_out, int* bi_out) {
+  if (!overflow_fits(pool, need)) return E_WORKSPACE;
   const bool small_ok = pool.nbig > 0 && need + need / 2 <= pool.big_bytes;
   const bool large_ok = pool.nbig2 > 0 && need <= pool.big2_bytes;
   const bool only_small = pool.nbig2 == 0;
@@ -268,7 +276,8 @@ HDN Arena overflow_acquire(const Ctx& c, const ttgbf_run_cfg& pool, int64_t need
   cls = (int)bcast_i(c, cls);
   *cls_out = cls;
   *bi_out = bi;
-  return cls == 0 ? make_ws_arena(pool.big_ws, pool.big_bytes, bi) : make_ws_arena(pool.big2_ws, pool.big2_bytes, bi);
+  *big = cls == 0 ? make_ws_arena(pool.big_ws, pool.big_bytes, bi) : make_ws_arena(pool.big2_ws, pool.big2_bytes, bi);
+  return OK;
 }
 
 HDN void overflow_release(const Ctx& c, const ttgbf_run_cfg& pool, const Arena& big, int cls, int bi,
@@ -346,9 +355,11 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
       int64_t nd = pb + pb / 16 + ((int64_t)64 << 20);
       if (nd < (int64_t)ar.cap) nd = (int64_t)ar.cap;
       int cls, bi;
-      Arena big = overflow_acquire(c, *pool, nd, dg, &cls, &bi);
-      hst = had_fin(big);
-      overflow_release(c, *pool, big, cls, bi, dg);
+      Arena big;
+      if (overflow_acquire(c, *pool, nd, dg, &big, &cls, &bi) == OK) {
+        hst = had_fin(big);
+        overflow_release(c, *pool, big, cls, bi, dg);
+      }
     }
     CK(hst);
     p = tt_view(hdr, state);
@@ -377,7 +388,8 @@ HDN int conv_in_overflow(const Ctx& c, Arena& ar, size_t mark, const TT& ker, co
                          const ttgbf_grid_cfg& gcfg, const ttgbf_run_cfg& pool, int64_t need, ttgbf_diag* dg,
                          TT& conv, double* sm) {
   int cls, bi;
-  Arena big = overflow_acquire(c, pool, need, dg, &cls, &bi);
+  Arena big;
+  CK(overflow_acquire(c, pool, need, dg, &big, &cls, &bi));
   TT big_conv;
   int st = tt_fft_conv(c, big, ker, shifted, gcfg.round_tol, gcfg.round_max_rank, big_conv, sm);
   if (!st) {
@@ -450,9 +462,6 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
     }
   }
   if (cst != OK) {
-    const bool fits = (pool->nbig > 0 && nd + nd / 2 <= pool->big_bytes) ||
-                      (pool->nbig2 > 0 && nd <= pool->big2_bytes) || (pool->nbig2 == 0 && nd <= pool->big_bytes);
-    if (!fits) return E_WORKSPACE;
     cst = conv_in_overflow(c, ar, m0, ker, shifted, gcfg, *pool, nd, dg, conv, S.sm);
     if (cst == E_WORKSPACE && pool->nbig2 > 0 && pool->big2_bytes > pool->big_bytes && nd + nd / 2 <= pool->big_bytes)
       cst = conv_in_overflow(c, ar, m0, ker, shifted, gcfg, *pool, pool->big_bytes + 1, dg, conv, S.sm);   // large class
@@ -462,7 +471,7 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   t0 = clk();
   int maxr = 1;
   for (int k = 0; k <= d; ++k) maxr = imax(maxr, conv.r[k]);
-  if (maxr > 512) return E_ARG;
+  if (maxr > CHAIN_MAXR) return E_ARG;
   // realign cross on the predictive grid
   if (c.leader()) {
     spec_grid(*sp, d, apd, io.pred);
@@ -600,7 +609,10 @@ HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
                                 io->pred)) {
         gst = E_ARG;
       } else {
-        for (int i = 0; i < d; ++i) { R->mean[i] = go->mean[i]; R->cov_diag[i] = go->cov[i * d + i]; }
+        for (int i = 0, q = 0; i < d; ++i) {
+          R->mean[i] = go->mean[i];
+          for (int j = i; j < d; ++j) R->cov[q++] = go->cov[i * d + j];
+        }
         R->spd_fixed = go->spd_fixed;
       }
     }

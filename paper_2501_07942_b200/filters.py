@@ -27,6 +27,8 @@ evaluates; an arbitrary Python callable is rejected (no CPU fallback).
 
 from __future__ import annotations
 
+from collections import OrderedDict
+
 import math
 from dataclasses import dataclass, field, replace
 
@@ -139,24 +141,48 @@ class PmdEstimate:
 # ---------------------------------------------------------------------------
 # engine access: one cached single-filter bank per (model, configs)
 # ---------------------------------------------------------------------------
-_BANKS: dict = {}
+_BANK_LIMIT = 4                       # banks kept alive (LRU); each owns device workspaces
+_BANKS: "OrderedDict[tuple, FilterBank]" = OrderedDict()
 _PLACEHOLDERS: dict = {}
 
 
+def _spec_key(spec) -> tuple:
+    """Content key of a model spec: two StateSpaceModel objects with the same
+    F, Q, R, h, H and angle components share one engine bank."""
+    out = []
+    for name in sorted(spec):
+        v = spec[name]
+        if isinstance(v, np.ndarray):
+            out.append((name, v.shape, v.dtype.str, v.tobytes()))
+        elif isinstance(v, (list, tuple)):
+            out.append((name, tuple(v)))
+        else:
+            out.append((name, v))
+    return tuple(out)
+
+
 def _bank(model: StateSpaceModel, cfg: GridConfig, cross: CrossConfig) -> FilterBank:
-    key = (id(model), cfg, cross.tol, cross.max_rank, cross.max_sweeps, cross.rng_seed,
+    key = (_spec_key(model.spec), cfg, cross.tol, cross.max_rank, cross.max_sweeps, cross.rng_seed,
            cross.validation_count, cross.cache_cap)
     b = _BANKS.get(key)
-    if b is None:
-        bc = BankConfig(n_per_axis=cfg.n_per_axis, sigma_mult=cfg.sigma_mult, round_tol=cfg.round_tol,
-                        round_max_rank=cfg.round_max_rank, normalize_before_round=cfg.normalize_before_round,
-                        densify_guard=cfg.densify_guard, tol=cross.tol, max_rank=cross.max_rank,
-                        max_sweeps=cross.max_sweeps, rng_seed=cross.rng_seed,
-                        validation_count=cross.validation_count, cache_cap=cross.cache_cap)
-        b = FilterBank(model.spec, bc, 1)
-        _BANKS[key] = b
-        b._model_ref = model   # keep id() stable
+    if b is not None:
+        _BANKS.move_to_end(key)
+        return b
+    bc = BankConfig(n_per_axis=cfg.n_per_axis, sigma_mult=cfg.sigma_mult, round_tol=cfg.round_tol,
+                    round_max_rank=cfg.round_max_rank, normalize_before_round=cfg.normalize_before_round,
+                    densify_guard=cfg.densify_guard, tol=cross.tol, max_rank=cross.max_rank,
+                    max_sweeps=cross.max_sweeps, rng_seed=cross.rng_seed,
+                    validation_count=cross.validation_count, cache_cap=cross.cache_cap)
+    while len(_BANKS) >= _BANK_LIMIT:
+        _BANKS.popitem(last=False)       # frees the evicted bank's device buffers
+    b = FilterBank(model.spec, bc, 1)
+    _BANKS[key] = b
     return b
+
+
+def release_banks() -> None:
+    """Drop every cached engine bank (and its device memory)."""
+    _BANKS.clear()
 
 
 def _raise(status: int, where: str):
@@ -164,7 +190,7 @@ def _raise(status: int, where: str):
         raise DegenerateDensityError(f"{where}: TT weights carry no probability mass")
     if status in (_abi.E_ARG, _abi.E_NONFINITE):
         raise ValueError(f"{where}: {_abi.status_text(status)}")
-    raise MemoryError(f"{where}: {_abi.status_text(status)}") if status in (_abi.E_WORKSPACE, _abi.E_CACHE) \
+    raise MemoryError(f"{where}: {_abi.status_text(status)}") if status in (_abi.E_WORKSPACE, _abi.E_CACHE, _abi.E_STATE_CAP) \
         else RuntimeError(f"{where}: {_abi.status_text(status)}")
 
 

@@ -259,6 +259,187 @@ def dense():
     np.savez_compressed(os.path.join(HERE, "dense.npz"), **out)
 
 
+class _BigKeyEvaluator(rta._CachedEvaluator):
+    """The reference's _CachedEvaluator (tt_algorithms.py:137-208) with its
+    int64 ``ravel_multi_index`` key replaced by the exact C-order flat index
+    as a Python int.  d=10, N=129 (BASELINE config 4) has 129**10 > 2**63
+    cells, so the stock class raises in ``initial_pmd_tt``; this is the ONLY
+    change (keys still sort ascending in C order, misses are still appended
+    sorted-unique, ``sample_cache`` still draws positions with the same rng
+    call), so every decision of ``greedy_cross`` is otherwise the reference's.
+    Used for config 4 only."""
+
+    def __init__(self, bb):
+        super().__init__(bb)
+        w = [1] * len(self._shape)
+        for k in range(len(self._shape) - 2, -1, -1):
+            w[k] = w[k + 1] * int(self._shape[k + 1])
+        self._w = w
+        self._keys: list[int] = []
+
+    def _flat(self, idx):
+        return [sum(int(i) * w for i, w in zip(row, self._w)) for row in idx.tolist()]
+
+    def _unflat(self, keys):
+        out = np.empty((len(keys), len(self._shape)), dtype=np.intp)
+        for j, key in enumerate(keys):
+            for k, w in enumerate(self._w):
+                out[j, k], key = divmod(key, w)
+        return out
+
+    def __call__(self, idx):
+        idx = np.asarray(idx, dtype=np.intp).reshape(-1, len(self._shape))
+        keys = self._flat(idx)
+        miss = sorted({k for k in keys if k not in self._pos})
+        if miss:
+            arr = self._unflat(miss)
+            vals = np.asarray(self._bb.evaluate_many(arr), dtype=float).reshape(-1)
+            if vals.shape != (len(miss),):
+                raise ValueError("evaluator returned wrong number of values")
+            if not np.all(np.isfinite(vals)):
+                raise ValueError("evaluator returned a non-finite value")
+            self.calls += len(miss)
+            if len(vals):
+                self.max_abs = max(self.max_abs, float(np.max(np.abs(vals))))
+            need = self._count + len(miss)
+            self._grow(need)
+            self._val_buf[self._count: need] = vals
+            self._pos.update(zip(miss, range(self._count, need)))
+            self._keys.extend(miss)
+            self._count = need
+        return self._val_buf[np.array([self._pos[k] for k in keys], dtype=np.int64)]
+
+    def sample_cache(self, rng, count):
+        if self._count > count:
+            sel = rng.choice(self._count, size=count, replace=False)
+        else:
+            sel = np.arange(self._count)
+        return self._unflat([self._keys[j] for j in sel]), self._val_buf[sel].copy()
+
+
+BASELINE_RUNS = {"C3": (8, 2), "C2": (8, 2), "C1": (8, 3), "C4": (8, 2)}
+SAMPLE_SEED = 12345
+SAMPLE_COUNT = 10_000
+
+
+def sample_indices(shape):
+    """The 10^4 seeded grid indices at which densities are compared (north star)."""
+    rng = np.random.default_rng(SAMPLE_SEED)
+    return np.stack([rng.integers(0, n, SAMPLE_COUNT) for n in shape], axis=1)
+
+
+def _perturbed_cross(seed):
+    """greedy_cross whose black box returns v * (1 + s * 2**-52), s in {-1, 0, 1}
+    a deterministic hash of the multi-index: the
+    reference's own sensitivity to one-ulp evaluator differences."""
+    stock = rta.greedy_cross
+    w = np.array([1000003, 10007, 101, 7919, 31, 13, 3, 17, 5, 29, 7, 11, 19, 23, 37, 41], dtype=np.int64)
+
+    def wrapped(bb, cfg):
+        inner = bb.evaluate_many
+
+        def ev(idx):
+            idx = np.asarray(idx, dtype=np.int64)
+            v = np.asarray(inner(idx), dtype=float)
+            s = ((idx @ w[: idx.shape[1]] + seed) % 3) - 1
+            return v * (1.0 + s * 2.0 ** -52)
+
+        return stock(rta.BlackBoxTensor(shape=bb.shape, evaluate_many=ev), cfg)
+    return wrapped
+
+
+def baseline_band():
+    """The same runs as baseline() with ulp-perturbed evaluators (two hash
+    seeds): tests/golden/baseline_band.npz.  |perturbed - baseline| per
+    (run, step) is the reference's self-disagreement band (Appendix A.3)."""
+    stock_f, stock_a = rf.greedy_cross, rta.greedy_cross
+    out = {}
+    try:
+        for seed in (1, 2):
+            rf.greedy_cross = _perturbed_cross(seed)
+            part = baseline(write=False)
+            out.update({f"p{seed}/{k}": v for k, v in part.items()})
+    finally:
+        rf.greedy_cross, rta.greedy_cross = stock_f, stock_a
+    np.savez_compressed(os.path.join(HERE, "baseline_band.npz"), **out)
+
+
+def baseline(write=True):
+    """Full tt_fft_pmf_step goldens on the BASELINE configs with
+    the metric cross (configs.METRIC_CROSS): per run (trajectory seed
+    SeedSequence((2024, run, 0))), per step: filtered moments, grid axes,
+    diagnostics, cross info, output ranks and the output density at 10^4
+    seeded indices; the step at which DegenerateDensityError fired, if any.
+    Config 4 runs with _BigKeyEvaluator (see its docstring)."""
+    from paper_2501_07942_b200.configs import BASELINE_CONFIGS
+    only = os.environ.get("BASELINE_ONLY")
+    path = os.path.join(HERE, "baseline.npz")
+    out = dict(np.load(path)) if (write and only and os.path.exists(path)) else {}
+    stock = rta._CachedEvaluator
+    for name, (runs, steps) in BASELINE_RUNS.items():
+        if only and name not in only.split(","):
+            continue
+        for key in [k for k in out if k.startswith(name + "/")]:
+            del out[key]
+        cfg = BASELINE_CONFIGS[name]
+        spec = cfg["spec"]
+        m = ref_model(spec)
+        gcfg = rf.GridConfig(**cfg["grid"])
+        ccfg = rta.CrossConfig(**cfg["cross"])
+        d = spec["F"].shape[0]
+        idx = sample_indices((cfg["grid"]["n_per_axis"],) * d)
+        out[f"{name}/idx"] = idx
+        rta._CachedEvaluator = _BigKeyEvaluator if name == "C4" else stock
+        try:
+            for run in range(runs):
+                traj = rm.simulate(m, cfg["x0_mean"], cfg["x0_cov"], cfg["steps"],
+                                   seed=np.random.SeedSequence((2024, run, 0)))
+                key = f"{name}/{run}"
+                out[f"{key}/z"] = traj.measurements[:steps]
+                t0 = time.time()
+                try:
+                    pmd = rf.initial_pmd_tt(MomentEstimate(cfg["x0_mean"], cfg["x0_cov"]), gcfg, ccfg)
+                except rf.DegenerateDensityError:
+                    out[f"{key}/done"] = np.array(-1)
+                    continue
+                out[f"{key}/init/ranks"] = np.array(pmd.weights.ranks)
+                out[f"{key}/init/sample"] = rtt.tt_eval_many(pmd.weights, idx)
+                out[f"{key}/init/cross"] = np.array(list(pmd.diag.cross_info["initial_pmd"]), dtype=float)
+                done = 0
+                times = []
+                for k in range(steps):
+                    ts = time.time()
+                    try:
+                        pmd = rf.tt_fft_pmf_step(pmd, m, traj.measurements[k], gcfg, ccfg)
+                    except rf.DegenerateDensityError:
+                        break
+                    times.append(time.time() - ts)
+                    dg = pmd.diag
+                    sk = f"{key}/{k}"
+                    out[f"{sk}/filt_mean"] = dg.filt_moments.mean
+                    out[f"{sk}/filt_cov"] = dg.filt_moments.cov
+                    out[f"{sk}/axes"] = np.stack(pmd.grid.axes)
+                    out[f"{sk}/diag"] = np.array([dg.mass_before_norm, dg.clipped_mass, float(dg.outlier),
+                                                  float(dg.spd_fixed)])
+                    out[f"{sk}/cross"] = np.array([list(dg.cross_info[c]) for c in
+                                                   ("likelihood", "kernel", "realign")], dtype=float)
+                    out[f"{sk}/ranks"] = np.array(pmd.weights.ranks)
+                    out[f"{sk}/sample"] = rtt.tt_eval_many(pmd.weights, idx)
+                    out[f"{sk}/sum"] = np.array(float(rtt.tt_sum(pmd.weights)))
+                    done += 1
+                out[f"{key}/done"] = np.array(done)
+                out[f"{key}/seconds"] = np.array(times)
+                print(name, run, "steps", done, "fail" if done < steps else "",
+                      " ".join("%.1fs" % t for t in times), "total %.1fs" % (time.time() - t0), flush=True)
+        finally:
+            rta._CachedEvaluator = stock
+        out[f"{name}/runs"] = np.array(runs)
+        out[f"{name}/steps"] = np.array(steps)
+    if write:
+        np.savez_compressed(path, **out)
+    return out
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["primitives", "crosses", "models", "trajectories", "dense", "standard"]
     for w in which:

@@ -106,26 +106,50 @@ def check_primitives(golden, case):
 
 
 
-def compare_scenario_run(golden, name, backend):
-    """The persistent multi-step kernel (device geometry) on a golden scenario."""
+def compare_scenario_run(golden, name, backend, **bank_kw):
+    """The persistent multi-step kernel (device geometry) on a golden scenario:
+    per step the filtered mean and full covariance, mass_before_norm,
+    clipped_mass and the three cross call counts; the final density and ranks."""
+    from paper_2501_07942_b200 import _abi
     z = golden("trajectories")
     sc = SCENARIOS[name]
-    bank = FilterBank(sc["spec"], bank_config(sc), 1, backend=backend)
+    bank = FilterBank(sc["spec"], bank_config(sc, **bank_kw), 1, backend=backend)
     done = int(z[f"{name}/done"])
     zs = z[f"{name}/z"][None, :, :]
     recs = bank.run(zs, done, sc["x0_mean"], sc["x0_cov"])[0]
+    d = sc["spec"]["F"].shape[0]
+    covs = _abi.rec_cov(recs, d)
     rows = []
     for k in range(done):
         r = recs[k]
         assert int(r["status"]) == 0 and int(r["k"]) == k, (k, r["status"], r["k"])
-        d = sc["spec"]["F"].shape[0]
+        ref_diag = z[f"{name}/{k}/diag"]
         rows.append({"step": k, "mean": rel(r["mean"][:d], z[f"{name}/{k}/filt_mean"]),
-                     "cov": rel(r["cov_diag"][:d], np.diag(z[f"{name}/{k}/filt_cov"]))})
+                     "cov": rel(covs[k], z[f"{name}/{k}/filt_cov"]),
+                     "mass_before_norm": abs(float(r["mass_before_norm"]) - ref_diag[0]) / abs(ref_diag[0]),
+                     "clipped_mass": abs(float(r["clipped_mass"]) - ref_diag[1]) / max(1.0, abs(ref_diag[1])),
+                     "calls": (tuple(int(v) for v in r["calls"]),
+                               tuple(int(v) for v in z[f"{name}/{k}/cross"][:, 1]))})
     got = bank.cores(0)
     ref = load_tt(z, f"{name}/{done - 1}/pred")
     rows.append({"step": "final", "dens": rel(T.to_full(got), T.to_full(ref)),
                  "ranks": (T.ranks_of(got), T.ranks_of(ref))})
     return rows
+
+
+RUN_TOL = {"mean": 1e-8, "cov": 1e-7, "dens": 1e-7, "mass_before_norm": 1e-8, "clipped_mass": 1e-9}
+
+
+def check_run(rows, calls=True):
+    for r in rows:
+        for key, tol in RUN_TOL.items():
+            if key in r:
+                assert r[key] <= tol, (r, key)
+        if "ranks" in r:
+            assert r["ranks"][0] == r["ranks"][1], r
+        if calls and "calls" in r:   # counts follow pivot ties at roundoff level: 10 %
+            for a, b in zip(*r["calls"]):
+                assert abs(a - b) <= 0.1 * b, r
 
 
 def check_large_eval(golden, case):
@@ -146,3 +170,107 @@ def check_large_eval(golden, case):
     og = Grid(geo.grid_from_bounds([o[0] for o in old], [o[-1] for o in old], list(shape)))
     pts = np.column_stack([rng.uniform(ax[0] - 0.2, ax[-1] + 0.2, 5000) for ax in og.axes])
     assert rel(G.tt_eval_at_points(a, og, pts), T.at_points(cores, og.axes, pts)) <= 1e-13
+
+
+# ---------------------------------------------------------------------------
+# BASELINE-config goldens (tests/golden/baseline.npz, make_golden.baseline):
+# full tt_fft_pmf_step runs of the real reference on configs C1-C4.
+# ---------------------------------------------------------------------------
+def baseline_bank(cfg_name, count, backend, **kw):
+    from paper_2501_07942_b200.configs import BASELINE_CONFIGS
+    cfg = BASELINE_CONFIGS[cfg_name]
+    g, x = cfg["grid"], cfg["cross"]
+    base = dict(n_per_axis=g["n_per_axis"], sigma_mult=g["sigma_mult"], round_tol=g["round_tol"],
+                round_max_rank=g["round_max_rank"], tol=x["tol"], max_rank=x["max_rank"], rng_seed=x["rng_seed"],
+                ws_bytes=1 << 30, state_doubles=1 << 20, cache_cap=1 << 21)
+    base.update(kw)
+    return cfg, FilterBank(cfg["spec"], BankConfig(**base), count, backend=backend)
+
+
+def compare_baseline(golden, cfg_name, backend, persistent=False, runs=None, **bank_kw):
+    """Run the golden runs of one BASELINE config as one filter bank, through
+    the stage API (bank.step: measure launch, host geometry, time-update
+    launch) or the persistent kernel (bank.run one step per launch, device
+    geometry).  Returns one row per (run, step) the reference attempted."""
+    from paper_2501_07942_b200 import _abi
+    z = golden("baseline")
+    nruns, steps = int(z[f"{cfg_name}/runs"]), int(z[f"{cfg_name}/steps"])
+    runs = list(range(nruns)) if runs is None else list(runs)
+    idx = z[f"{cfg_name}/idx"]
+    cfg, bank = baseline_bank(cfg_name, len(runs), backend, **bank_kw)
+    d = cfg["spec"]["F"].shape[0]
+    Z = np.stack([z[f"{cfg_name}/{r}/z"] for r in runs])
+    done = [int(z[f"{cfg_name}/{r}/done"]) for r in runs]
+    rows = []
+    if not persistent:
+        dg = bank.init_prior(cfg["x0_mean"], cfg["x0_cov"])
+        for j, r in enumerate(runs):
+            key = f"{cfg_name}/{r}/init"
+            assert int(dg["status"][j]) == 0, (r, dg["status"][j])
+            got = bank.cores(j)
+            rows.append({"run": r, "step": -1, "ranks": (T.ranks_of(got), tuple(z[f"{key}/ranks"])),
+                         "dens": rel(T.at_indices(got, idx), z[f"{key}/sample"]),
+                         "calls": (int(dg["cross"][j][0]["calls"]), int(z[f"{key}/cross"][1]))})
+    alive = np.ones(len(runs), dtype=bool)
+    for k in range(steps):
+        if persistent:
+            recs = bank.run(Z, 1, cfg["x0_mean"], cfg["x0_cov"])[:, 0]
+            status = recs["status"]
+            covs = _abi.rec_cov(recs, d)
+        else:
+            res = bank.step(Z[:, k])
+            status = res["status"]
+            dt = res["time"]
+        for j, r in enumerate(runs):
+            if not alive[j] or k > done[j]:
+                continue
+            sk = f"{cfg_name}/{r}/{k}"
+            failed_ref = k == done[j]
+            row = {"run": r, "step": k, "status": (int(status[j]), failed_ref)}
+            if not failed_ref and int(status[j]) == 0:
+                got = bank.cores(j)
+                ref_diag = z[f"{sk}/diag"]
+                ref_cross = z[f"{sk}/cross"]
+                if persistent:
+                    mean, cov = recs["mean"][j][:d], covs[j]
+                    mb, cm = float(recs["mass_before_norm"][j]), float(recs["clipped_mass"][j])
+                    calls = tuple(int(v) for v in recs["calls"][j])
+                else:
+                    mean, cov = res["mean"][j], res["cov"][j]
+                    mb, cm = float(dt["mass_before_norm"][j]), float(dt["clipped_mass"][j])
+                    calls = (int(res["measure"]["cross"][j][0]["calls"]),) + \
+                        tuple(int(dt["cross"][j][q]["calls"]) for q in (1, 2))
+                row.update({
+                    "mean": rel(mean, z[f"{sk}/filt_mean"]), "cov": rel(cov, z[f"{sk}/filt_cov"]),
+                    "dens": rel(T.at_indices(got, idx), z[f"{sk}/sample"]),
+                    "ranks": (T.ranks_of(got), tuple(z[f"{sk}/ranks"])),
+                    "axes": rel(np.stack(bank.grids[j].axes()), z[f"{sk}/axes"]),
+                    "mass_before_norm": abs(mb - ref_diag[0]) / abs(ref_diag[0]),
+                    "clipped_mass": abs(cm - ref_diag[1]) / max(1.0, abs(ref_diag[1])),
+                    "calls": (calls, tuple(int(v) for v in ref_cross[:, 1])),
+                })
+            rows.append(row)
+            if int(status[j]) != 0 or failed_ref:
+                alive[j] = False
+    return rows
+
+
+BASELINE_TOL = {"mean": 1e-8, "cov": 1e-7, "dens": 1e-7, "axes": 1e-8, "mass_before_norm": 1e-8,
+                "clipped_mass": 1e-9}
+
+
+def check_baseline(rows):
+    bad = []
+    for r in rows:
+        if "status" in r:
+            st, failed_ref = r["status"]
+            if (st != 0) != failed_ref:
+                bad.append((r["run"], r["step"], "status", st, failed_ref))
+                continue
+        for key, tol in BASELINE_TOL.items():
+            if key in r and not r[key] <= tol:
+                bad.append((r["run"], r["step"], key, r[key]))
+        for key in ("ranks", "calls"):
+            if key in r and r[key][0] != r[key][1]:
+                bad.append((r["run"], r["step"], key, r[key]))
+    assert not bad, bad

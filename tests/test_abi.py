@@ -34,3 +34,13 @@ def test_library_exports_header():
     assert lib.ttgbf_version() == 1
     assert lib.ttgbf_status_string(3) == b"TT weights carry no probability mass"
     assert lib.ttgbf_dense_reduce_blocks() > 0
+
+
+def test_struct_layouts_match_header():
+    """Every ABI struct mirror has the size the compiled library reports."""
+    from paper_2501_07942_b200 import _abi
+    if not os.path.exists(_abi.PRODUCT_LIB):
+        pytest.skip("product library not built (run __graft_entry__.build())")
+    lib = _abi.bind(ctypes.CDLL(_abi.PRODUCT_LIB))
+    for which, size in _abi.struct_sizes().items():
+        assert lib.ttgbf_sizeof(which) == size, (which, lib.ttgbf_sizeof(which), size)

@@ -26,14 +26,8 @@ def test_primitives_hostsim(golden, backend, case):
 
 @pytest.mark.parametrize("name", ["scaling2_tight", "radar_deg", "identity2", "cv4_step0"])
 def test_persistent_run_hostsim(golden, backend, name):
-    from scenario_util import compare_scenario_run
-    rows = compare_scenario_run(golden, name, backend)
-    for r in rows:
-        for key, tol in (("mean", 1e-8), ("cov", 1e-7), ("dens", 1e-7)):
-            if key in r:
-                assert r[key] <= tol, r
-        if "ranks" in r:
-            assert r["ranks"][0] == r["ranks"][1], r
+    from scenario_util import check_run, compare_scenario_run
+    check_run(compare_scenario_run(golden, name, backend))
 
 
 @pytest.mark.parametrize("case", ["s3", "s4", "s6"])

@@ -71,3 +71,27 @@ def test_round_tall_cores_gpu(cuda, ranks, tol):
     got = G.tt_round(G.TensorTrain.from_cores(cores), tol)
     assert got.ranks == T.ranks_of(ref)
     assert rel(T.to_full(got.numpy_cores()), T.to_full(ref)) <= 1e-11
+
+
+@pytest.mark.parametrize("name", ["scaling2_tight", "radar_deg", "identity2", "cv4_step0"])
+def test_persistent_run_gpu(golden, cuda, name):
+    """The benchmarked path -- ttgbf_filter_run, one persistent launch with
+    device geometry (geom.cuh) -- against the reference's tier-3 trajectories:
+    filtered mean and full covariance every step, mass_before_norm,
+    clipped_mass, cross call counts, final density and ranks."""
+    from scenario_util import check_run, compare_scenario_run
+    check_run(compare_scenario_run(golden, name, cuda))
+
+
+@pytest.mark.parametrize("name", ["radar_deg", "cv4_step0"])
+def test_persistent_run_overflow_gpu(golden, cuda, name):
+    """Force the overflow workspaces: a slot too small for the FFT product /
+    Hadamard rounding makes the step redo that stage in a borrowed buffer
+    (spin-locked pool, both classes); the result must be the in-slot result."""
+    from scenario_util import check_run, compare_scenario_run
+    rows_small = compare_scenario_run(golden, name, cuda, ws_bytes=24 << 20, big_slots=1, big_bytes=256 << 20,
+                                      big2_slots=1, big2_bytes=512 << 20)
+    check_run(rows_small)
+    rows = compare_scenario_run(golden, name, cuda)
+    for a, b in zip(rows, rows_small):
+        assert a == b, (a, b)
