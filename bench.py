@@ -1,19 +1,21 @@
 """TT-GBF throughput bench (BASELINE.json metric: filter steps/s at d=6, N_pa=64 -> 65, rank <= 20).
 
-Workload (BASELINE config 5 = config 3 batched): independent seeded Monte Carlo
-filters of the d=6 constant-velocity model, ``--batch`` filters per GPU.  One
-bench *step* = one ``tt_fft_pmf_step`` for every filter of the batch (two
-kernel launches for the whole batch + the host-side grid geometry).  Filters
-that raise DegenerateDensityError are restarted from the prior before the next
-step (the restart is inside the timed region); only completed steps count.
+Workload (BASELINE config 5 = config 3 batched): the 4096 seeded Monte Carlo
+runs of the d=6 constant-velocity model, split evenly across the GPUs
+(strong scaling; ``--batch B`` instead fixes B filters per GPU).  One bench
+*step* = one ``tt_fft_pmf_step`` for every filter; all K timed steps of all
+filters run in ONE persistent ``ttgbf_filter_run`` launch (device geometry,
+per-step work claiming).  Filters that raise DegenerateDensityError restart
+from the prior inside the timed region; only completed steps count.
 
-  python bench.py [--gpus N --steps K --warmup W --batch B]
+  python bench.py [--gpus N --steps K --warmup W]
   python bench.py --impl reference ...   # the reference algorithm on the host cores
                                           # (oracle port; the Python reference cannot travel)
 
-Multi-GPU: one process per GPU (torchrun); runs are sharded by rank with no
-data-path collective; the per-run squared-error sums are gathered with one
-NCCL all_gather at the end.
+Multi-GPU: one process per GPU (``--gpus N`` re-launches itself under
+torch.distributed.run when WORLD_SIZE is unset); runs are sharded by rank
+with no data-path collective; the per-run squared-error sums are gathered
+with one NCCL all_gather at the end.
 """
 
 from __future__ import annotations
@@ -46,7 +48,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--batch", type=int, default=4096)  # filters per GPU (BASELINE config 5: 4096 trajectories)
+    p.add_argument("--runs", type=int, default=0)     # total Monte Carlo runs (0: the config's, C5 = 4096)
+    p.add_argument("--batch", type=int, default=0)    # filters per GPU (0: runs / GPUs, BASELINE config 5)
     p.add_argument("--slots", type=int, default=0)     # resident CTAs (0: SMs x ttgbf_ctas_per_sm)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C5")
@@ -127,43 +130,94 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU reference (oracle port of the reference algorithm)
 # ---------------------------------------------------------------------------
-def _oracle_worker(args):
-    cfg_name, run, budget_s = args
+_W = {}   # per-process oracle filter state of the CPU reference arm
+
+
+def _oracle_init(cfg_name, worker, stride):
+    """Worker state: runs worker, worker + stride, ... of the config, each from
+    the prior with its own SeedSequence((2024, run, 0)) trajectory."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    _W.update(cfg=cfg_name, run=worker - stride, stride=stride, state=None)
+
+
+def _oracle_new_run():
     from oracle import pmf
-    cfg = BASELINE_CONFIGS[cfg_name]
-    g = {"n_per_axis": cfg["grid"]["n_per_axis"], "sigma_mult": cfg["grid"]["sigma_mult"],
-         "round_tol": cfg["grid"]["round_tol"], "round_max_rank": cfg["grid"]["round_max_rank"]}
-    _, meas = simulate(cfg["spec"], cfg["x0_mean"], cfg["x0_cov"], cfg["steps"], np.random.SeedSequence((2024, run, 0)))
-    done, k = 0, 0
-    t0 = time.perf_counter()
+    cfg = BASELINE_CONFIGS[_W["cfg"]]
+    _W["run"] += _W["stride"]
+    _, meas = simulate(cfg["spec"], cfg["x0_mean"], cfg["x0_cov"], cfg["steps"],
+                       np.random.SeedSequence((2024, _W["run"], 0)))
+    g = _W["g"] = {"n_per_axis": cfg["grid"]["n_per_axis"], "sigma_mult": cfg["grid"]["sigma_mult"],
+                   "round_tol": cfg["grid"]["round_tol"], "round_max_rank": cfg["grid"]["round_max_rank"]}
     axes, cores, _ = pmf.initial(cfg["x0_mean"], cfg["x0_cov"], g, cfg["cross"])
-    while time.perf_counter() - t0 < budget_s:
+    _W["state"] = [axes, cores, 0, meas]
+
+
+def _oracle_restart():
+    from oracle import pmf
+    cfg = BASELINE_CONFIGS[_W["cfg"]]
+    axes, cores, _ = pmf.initial(cfg["x0_mean"], cfg["x0_cov"], _W["g"], cfg["cross"])
+    _W["state"][:3] = [axes, cores, 0]
+
+
+def _oracle_advance(arg):
+    """Run this worker's filters for ~budget_s (or exactly `steps` attempted
+    steps): the GPU arm's policy -- a failed step restarts its filter from the
+    prior, a finished trajectory moves to the worker's next run.  Returns
+    (completed steps, seconds)."""
+    budget_s, steps = arg
+    from oracle import pmf
+    cfg = BASELINE_CONFIGS[_W["cfg"]]
+    done = att = 0
+    t0 = time.perf_counter()
+    if _W["state"] is None:
+        _oracle_new_run()
+    while (steps and att < steps) or (not steps and time.perf_counter() - t0 < budget_s):
+        axes, cores, k, meas = _W["state"]
+        att += 1
         try:
-            axes, cores, _ = pmf.step(axes, cores, cfg["spec"], meas[k], g, cfg["cross"])
+            axes, cores, _ = pmf.step(axes, cores, cfg["spec"], meas[k], _W["g"], cfg["cross"])
             done += 1
-            k += 1
+            _W["state"][:3] = [axes, cores, k + 1]
+            if k + 1 >= cfg["steps"]:
+                _oracle_new_run()
         except pmf.Degenerate:
-            axes, cores, _ = pmf.initial(cfg["x0_mean"], cfg["x0_cov"], g, cfg["cross"])
-            k = 0
-        if k >= cfg["steps"]:
-            axes, cores, _ = pmf.initial(cfg["x0_mean"], cfg["x0_cov"], g, cfg["cross"])
-            k = 0
+            _oracle_restart()
     return done, time.perf_counter() - t0
+
+
+class CpuReference:
+    """The reference algorithm (oracle port) on `cores` host processes, one
+    filter stream each (runs interleaved across workers), state kept across
+    samples so successive samples walk through the run set instead of
+    re-timing the same first steps."""
+
+    def __init__(self, cfg_name, cores):
+        import multiprocessing as mp
+        self.cores = cores
+        self.pools = [mp.get_context("spawn").Pool(1, _oracle_init, (cfg_name, w, cores)) for w in range(cores)]
+
+    def sample(self, budget_s=0.0, steps=0):
+        res = [p.apply_async(_oracle_advance, ((budget_s, steps),)) for p in self.pools]
+        out = [r.get() for r in res]
+        done = sum(o[0] for o in out)
+        wall = max(o[1] for o in out)
+        # aggregate rate = sum of the workers' own rates (a worker finishing a
+        # long step late does not idle the others in the count)
+        return sum(o[0] / o[1] for o in out if o[1] > 0), done, wall
+
+    def close(self):
+        for p in self.pools:
+            p.terminate()
 
 
 def cpu_reference(cfg_name, cores, budget_s):
     """Completed oracle steps/s over `cores` worker processes, each for ~budget_s."""
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    if cores == 1:
-        res = [_oracle_worker((cfg_name, 0, budget_s))]
-    else:
-        import multiprocessing as mp
-        with mp.get_context("spawn").Pool(cores) as pool:
-            res = pool.map(_oracle_worker, [(cfg_name, r, budget_s) for r in range(cores)])
-    done = sum(r[0] for r in res)
-    wall = max(r[1] for r in res)
-    return done / wall, done, wall
+    ref = CpuReference(cfg_name, cores)
+    try:
+        return ref.sample(budget_s)
+    finally:
+        ref.close()
 
 
 def run_reference(args):
@@ -171,22 +225,29 @@ def run_reference(args):
     if rank != 0:
         return
     cores = len(os.sched_getaffinity(0))
-    budget = max(5.0, min(60.0, 120.0 / max(1, args.steps + args.warmup)))
-    for _ in range(args.warmup):
-        cpu_reference(args.config, cores, budget / 4)
-    vals = []
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, done, wall = cpu_reference(args.config, cores, budget)
-        vals.append(v)
-    elapsed = time.perf_counter() - t0
+    budget = max(5.0, min(60.0, 150.0 / max(1, args.steps + args.warmup)))
+    ref = CpuReference(args.config, cores)
+    try:
+        # warm-up: every worker advances its first filter (the GPU arm's W warm-up steps)
+        ref.sample(steps=args.warmup)
+        vals = []
+        t0 = time.perf_counter()
+        done_total = 0
+        for _ in range(args.steps):
+            v, done, wall = ref.sample(budget)
+            vals.append(v)
+            done_total += done
+        elapsed = time.perf_counter() - t0
+    finally:
+        ref.close()
     value = float(np.mean(vals))
-    sample = (f"{args.steps} samples x {cores} processes x ~{budget:.0f}s of {args.config} oracle steps "
-              "(runs 0..cores-1 from the prior, restart on DegenerateDensityError)")
+    sample = (f"{args.steps} samples x {cores} processes x ~{budget:.0f}s of {args.config} oracle steps; "
+              f"{done_total} completed steps; each process walks its own runs (run = worker + {cores} j) "
+              f"after {args.warmup} untimed warm-up steps, restarting failed filters from the prior")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / max(1, args.steps),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded trajectories)",
         "config": {"workload": WORKLOAD, "parallelism": "host processes"},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample},
@@ -224,7 +285,10 @@ def run_ours(args):
 
     cfg = BASELINE_CONFIGS[args.config]
     g, x = cfg["grid"], cfg["cross"]
-    B = args.batch
+    from paper_2501_07942_b200.mc import shard
+    total_runs = args.batch * world if args.batch > 0 else (args.runs or int(cfg["runs"]))
+    runs = shard(total_runs, world, rank)          # strong scaling: the fixed C5 run set split across GPUs
+    B = len(runs)
     from paper_2501_07942_b200 import _abi
     lib = _abi.load_library()
     if args.slots <= 0:
@@ -241,8 +305,6 @@ def run_ours(args):
     d = cfg["spec"]["F"].shape[0]
     b = np.atleast_2d(cfg["spec"]["R"]).shape[0]
     n = g["n_per_axis"]
-    from paper_2501_07942_b200.mc import shard
-    runs = shard(world * B, world, rank)          # weak scaling: B filters per GPU
     states, meas = trajectories(cfg, runs)
     kf = cfg["steps"]
     dev = torch.device("cuda", local)
@@ -340,9 +402,9 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if args.batch <= 0 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded trajectories, SeedSequence((2024, run, 0)))",
-        "config": {"workload": WORKLOAD, "filters_per_gpu": B, "runs": world * B, "parallelism": f"dp{world}",
+        "config": {"workload": WORKLOAD, "filters_per_gpu": B, "runs": total_runs, "parallelism": f"dp{world}",
                    "workspace_slots": args.slots, "workspace_mb_per_slot": args.ws_mb,
                    "l2": "per-filter working sets stream from HBM (batch footprint >> 126 MB L2)",
                    "completed_steps": done_all, "restarts": stats["restarts"], "failed_steps": stats["failed"],
@@ -396,8 +458,22 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def self_launch(args) -> int:
+    """--gpus N outside torchrun: re-run this command as N ranks (one per GPU)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -140,8 +140,11 @@ typedef struct {
 } ttgbf_diag;
 
 /* Model constants (StateSpaceModel, models.py:85-153).  Matrices row-major
- * with leading dimension TTGBF_MAXD (F, Finv, Lq, H) or TTGBF_MAXB (Lr).
- * Lq / Lr are numpy's lower Cholesky factors of Q / R; logn_* the
+ * with leading dimension TTGBF_MAXD (F, Finv, LUq, H) or TTGBF_MAXB (LUr).
+ * LUq / LUr: LAPACK dgetrf factors of numpy's lower Cholesky factors of
+ * Q / R (what numpy.linalg.solve(chol, .) factors inside
+ * GaussianDensity.logpdf, models.py:60-63): row-major LU, 0-based sequential
+ * row swaps piv*, reciprocal pivots inv* = 1 / U_ii; logn_* the
  * GaussianDensity log normalisers (models.py:47-49). */
 typedef struct {
   int32_t d;
@@ -153,18 +156,25 @@ typedef struct {
   int32_t ang[TTGBF_MAXB];
   double F[TTGBF_MAXD * TTGBF_MAXD];
   double Finv[TTGBF_MAXD * TTGBF_MAXD];
-  double Lq[TTGBF_MAXD * TTGBF_MAXD];
+  double LUq[TTGBF_MAXD * TTGBF_MAXD];
+  int32_t pivq[TTGBF_MAXD];
+  double invq[TTGBF_MAXD];
   double logn_q;
-  double Lr[TTGBF_MAXB * TTGBF_MAXB];
+  double LUr[TTGBF_MAXB * TTGBF_MAXB];
+  int32_t pivr[TTGBF_MAXB];
+  double invr[TTGBF_MAXB];
   double logn_r;
   double H[TTGBF_MAXB * TTGBF_MAXD];
   double Q[TTGBF_MAXD * TTGBF_MAXD];
 } ttgbf_model;
 
-/* Gaussian prior (initial_pmd_tt) */
+/* Gaussian prior (initial_pmd_tt): mean, dgetrf factors of the covariance's
+ * lower Cholesky factor (as in ttgbf_model), log normaliser */
 typedef struct {
   double mean[TTGBF_MAXD];
-  double L[TTGBF_MAXD * TTGBF_MAXD];
+  double LU[TTGBF_MAXD * TTGBF_MAXD];
+  int32_t piv[TTGBF_MAXD];
+  double inv[TTGBF_MAXD];
   double logn;
 } ttgbf_gauss;
 

@@ -40,9 +40,11 @@ class CrossOut:
 class Memo:
     """Memoised counted evaluator.  tt_algorithms.py:137-208.
 
-    Keys are the C-order flat index held as Python ints (no int64 overflow).
-    Misses of a call are deduplicated, sorted ascending and appended in that
-    order -- the insertion order is what ``sample`` draws positions from.
+    Keys are the C-order flat index: int64 via ravel_multi_index (as the
+    reference computes them) when the grid has fewer than 2**63 cells, exact
+    Python ints otherwise (the reference overflows there, F6).  Misses of a
+    call are deduplicated, sorted ascending and appended in that order --
+    the insertion order is what ``sample`` draws positions from.
     """
 
     def __init__(self, shape, fn):
@@ -53,15 +55,23 @@ class Memo:
         self.vals = np.empty(1024)
         self.calls = 0
         self.max_abs = 0.0
+        self.small = math.prod(self.shape) < 2 ** 63
         w = [1] * len(self.shape)
         for k in range(len(self.shape) - 2, -1, -1):
             w[k] = w[k + 1] * self.shape[k + 1]
         self.weights = w
 
-    def flat(self, idx) -> list[int]:
+    def flat(self, idx):
+        if self.small:
+            return np.ravel_multi_index(tuple(np.asarray(idx, dtype=np.intp).T), self.shape)
         return [sum(int(i) * w for i, w in zip(row, self.weights)) for row in idx.tolist()]
 
     def unflat(self, keys) -> np.ndarray:
+        if self.small:
+            keys = np.asarray(keys, dtype=np.int64)
+            if keys.size == 0:
+                return np.empty((0, len(self.shape)), dtype=np.intp)
+            return np.column_stack(np.unravel_index(keys, self.shape)).astype(np.intp)
         out = np.empty((len(keys), len(self.shape)), dtype=np.intp)
         for j, key in enumerate(keys):
             for k, w in enumerate(self.weights):
@@ -70,8 +80,14 @@ class Memo:
 
     def __call__(self, idx) -> np.ndarray:
         idx = np.asarray(idx, dtype=np.intp).reshape(-1, len(self.shape))
-        keys = self.flat(idx)
-        miss = sorted({k for k in keys if k not in self.slot})
+        flat = self.flat(idx)
+        keys = flat.tolist() if self.small else flat
+        get = self.slot.get
+        if self.small:
+            pos = np.fromiter((get(k, -1) for k in keys), dtype=np.int64, count=len(keys))
+            miss = np.unique(flat[pos < 0]).tolist() if (pos < 0).any() else []
+        else:
+            miss = sorted({k for k in keys if k not in self.slot})
         if miss:
             v = np.asarray(self.fn(self.unflat(miss)), dtype=float).reshape(-1)
             if v.shape != (len(miss),):
@@ -86,10 +102,13 @@ class Memo:
                 grown[:base] = self.vals[:base]
                 self.vals = grown
             self.vals[base:base + len(miss)] = v
-            for j, k in enumerate(miss):
-                self.slot[k] = base + j
+            self.slot.update(zip(miss, range(base, base + len(miss))))
             self.keys.extend(miss)
-        return self.vals[np.array([self.slot[k] for k in keys], dtype=np.int64)]
+            if self.small:
+                pos = np.fromiter((get(k) for k in keys), dtype=np.int64, count=len(keys))
+        if not self.small:
+            pos = np.array([self.slot[k] for k in keys], dtype=np.int64)
+        return self.vals[pos]
 
     def sample(self, rng, count):
         n = len(self.keys)

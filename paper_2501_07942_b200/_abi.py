@@ -37,10 +37,12 @@ DIAG = np.dtype([("status", "i4"), ("outlier", "i4"), ("mass_before_norm", "f8")
                  ("prof", "i8", 32), ("big_used", "i8"), ("big_peak", "i8"),
                  ("big_wait", "i8")], align=True)
 MODEL = np.dtype([("d", "i4"), ("b", "i4"), ("hkind", "i4"), ("nang", "i4"), ("ang", "i4", MAXB),
-                  ("F", "f8", MAXD * MAXD), ("Finv", "f8", MAXD * MAXD), ("Lq", "f8", MAXD * MAXD),
-                  ("logn_q", "f8"), ("Lr", "f8", MAXB * MAXB), ("logn_r", "f8"),
+                  ("F", "f8", MAXD * MAXD), ("Finv", "f8", MAXD * MAXD), ("LUq", "f8", MAXD * MAXD),
+                  ("pivq", "i4", MAXD), ("invq", "f8", MAXD), ("logn_q", "f8"),
+                  ("LUr", "f8", MAXB * MAXB), ("pivr", "i4", MAXB), ("invr", "f8", MAXB), ("logn_r", "f8"),
                   ("H", "f8", MAXB * MAXD), ("Q", "f8", MAXD * MAXD)], align=True)
-GAUSS = np.dtype([("mean", "f8", MAXD), ("L", "f8", MAXD * MAXD), ("logn", "f8")], align=True)
+GAUSS = np.dtype([("mean", "f8", MAXD), ("LU", "f8", MAXD * MAXD), ("piv", "i4", MAXD), ("inv", "f8", MAXD),
+                  ("logn", "f8")], align=True)
 RUN_CFG_FIELDS = None
 STEP_REC = np.dtype([("status", "i4"), ("k", "i4"), ("spd_fixed", "i4"), ("outlier", "i4"), ("mean", "f8", MAXD),
                      ("cov", "f8", MAXD * (MAXD + 1) // 2), ("mass_before_norm", "f8"), ("clipped_mass", "f8"),
@@ -141,7 +143,10 @@ def struct_sizes() -> dict:
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(HERE, "_lib")
-PRODUCT_LIB = os.path.join(LIB_DIR, "libttgbf.so")
+# TTGBF_LIB_VARIANT=<tag> loads _lib/libttgbf_<tag>.so (a build of the same
+# sources with other compile-time tuning, e.g. CTAs per SM; tools/build_variant.sh)
+PRODUCT_LIB = os.path.join(LIB_DIR, "libttgbf%s.so" % (("_" + os.environ["TTGBF_LIB_VARIANT"])
+                                                       if os.environ.get("TTGBF_LIB_VARIANT") else ""))
 
 
 def bind(lib, dense: bool = True):

@@ -103,10 +103,16 @@ def model_record(spec) -> np.ndarray:
     if Finv is not None:
         put("Finv", Finv, _abi.MAXD)
     lq, nq = geo.gauss_consts(Q)
-    put("Lq", lq, _abi.MAXD)
+    luq, pq, iq = geo.solve_factors(lq)
+    put("LUq", luq, _abi.MAXD)
+    rec["pivq"][0, :d] = pq
+    rec["invq"][0, :d] = iq
     rec["logn_q"] = nq
     lr, nr = geo.gauss_consts(R)
-    put("Lr", lr, _abi.MAXB)
+    lur, pr, ir = geo.solve_factors(lr)
+    put("LUr", lur, _abi.MAXB)
+    rec["pivr"][0, :b] = pr
+    rec["invr"][0, :b] = ir
     rec["logn_r"] = nr
     if spec["h"] == "linear":
         put("H", np.atleast_2d(np.asarray(spec["H"], dtype=float)), _abi.MAXD)
@@ -117,12 +123,15 @@ def gauss_record(mean, cov) -> np.ndarray:
     rec = np.zeros(1, dtype=_abi.GAUSS)
     mean = np.asarray(mean, dtype=float).reshape(-1)
     L, logn = geo.gauss_consts(cov)
+    lu, piv, inv = geo.solve_factors(L)
     d = mean.size
     rec["mean"][0, :d] = mean
     buf = np.zeros(_abi.MAXD * _abi.MAXD)
     for i in range(d):
-        buf[i * _abi.MAXD: i * _abi.MAXD + d] = L[i]
-    rec["L"][0] = buf
+        buf[i * _abi.MAXD: i * _abi.MAXD + d] = lu[i]
+    rec["LU"][0] = buf
+    rec["piv"][0, :d] = piv
+    rec["inv"][0, :d] = inv
     rec["logn"] = logn
     return rec
 

@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(THREADS) k_prior(Geo g, const ttgbf_gauss* p, 
     unflat(g, e, idx);
     double x[MAXD];
     for (int k = 0; k < g.d; ++k) x[k] = axv(g.ax[k], idx[k]) - p->mean[k];
-    w[e] = exp(p->logn - 0.5 * tri_quad(p->L, g.d, MAXD, x));
+    w[e] = exp(p->logn - 0.5 * tri_quad(SolveLU{p->LU, p->piv, p->inv, MAXD}, g.d, x));
   }
 }
 
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(THREADS) k_likelihood(Geo g, const ttgbf_model
       const int a = m->ang[t];
       hz[a] = 180.0 - np_mod360(180.0 - hz[a]);
     }
-    w[e] = w[e] * exp(m->logn_r - 0.5 * tri_quad(m->Lr, s.b, MAXB, hz));
+    w[e] = w[e] * exp(m->logn_r - 0.5 * tri_quad(SolveLU{m->LUr, m->pivr, m->invr, MAXB}, s.b, hz));
   }
 }
 
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(THREADS) k_kernel(Geo g, const ttgbf_model* m,
       const int sg = idx[k] <= half ? idx[k] : idx[k] - g.n[k];
       disp[k] = (double)sg * steps[k];
     }
-    const double pdf = exp(m->logn_q - 0.5 * tri_quad(m->Lq, g.d, MAXD, disp));
+    const double pdf = exp(m->logn_q - 0.5 * tri_quad(SolveLU{m->LUq, m->pivq, m->invq, MAXD}, g.d, disp));
     out[e] = make_double2(pdf * cv / absdet, 0.0);
   }
 }

@@ -181,7 +181,8 @@ HD void spec_grid(EvalSpec& s, int d, double* const* axes, const ttgbf_axis* g) 
 
 HD void spec_prior(EvalSpec& s, const ttgbf_gauss& p) {
   s.kind = EV_GAUSS;
-  for (int i = 0; i < MAXD * MAXD; ++i) s.L[i] = p.L[i];
+  for (int i = 0; i < MAXD * MAXD; ++i) s.LU[i] = p.LU[i];
+  for (int i = 0; i < MAXD; ++i) { s.piv[i] = p.piv[i]; s.inv[i] = p.inv[i]; }
   for (int i = 0; i < MAXD; ++i) s.mean[i] = p.mean[i];
   s.log_norm = p.logn;
 }
@@ -192,14 +193,16 @@ HD void spec_likelihood(EvalSpec& s, const ttgbf_model& m, const double* z) {
   s.b = m.b;
   s.nang = m.nang;
   for (int i = 0; i < MAXB; ++i) { s.ang[i] = m.ang[i]; s.z[i] = z[i]; }
-  for (int i = 0; i < MAXB * MAXB; ++i) s.Lr[i] = m.Lr[i];
+  for (int i = 0; i < MAXB * MAXB; ++i) s.LUr[i] = m.LUr[i];
+  for (int i = 0; i < MAXB; ++i) { s.pivr[i] = m.pivr[i]; s.invr[i] = m.invr[i]; }
   for (int i = 0; i < MAXB * MAXD; ++i) s.H[i] = m.H[i];
   s.log_norm_r = m.logn_r;
 }
 
 HD void spec_kernel(EvalSpec& s, const ttgbf_model& m, const double* steps) {
   s.kind = EV_KERNEL;
-  for (int i = 0; i < MAXD * MAXD; ++i) { s.F[i] = m.F[i]; s.L[i] = m.Lq[i]; }
+  for (int i = 0; i < MAXD * MAXD; ++i) { s.F[i] = m.F[i]; s.LU[i] = m.LUq[i]; }
+  for (int i = 0; i < MAXD; ++i) { s.piv[i] = m.pivq[i]; s.inv[i] = m.invq[i]; }
   s.log_norm = m.logn_q;
   for (int k = 0; k < s.d; ++k) s.steps[k] = steps[k];
   s.cellvol = cell_volume(steps, s.d);
@@ -523,7 +526,8 @@ HDN int stage_time_std(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
       sp->n[d + k] = io.cur[k].n;
       sp->axes[d + k] = ao[k];
     }
-    for (int i = 0; i < MAXD * MAXD; ++i) { sp->F[i] = model.F[i]; sp->L[i] = model.Lq[i]; }
+    for (int i = 0; i < MAXD * MAXD; ++i) { sp->F[i] = model.F[i]; sp->LU[i] = model.LUq[i]; }
+    for (int i = 0; i < MAXD; ++i) { sp->piv[i] = model.pivq[i]; sp->inv[i] = model.invq[i]; }
     sp->log_norm = model.logn_q;
     sp->cellvol = cv_old;
   }

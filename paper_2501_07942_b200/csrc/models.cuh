@@ -7,7 +7,8 @@
 //   EV_TRANSITION N(x_new - F x_old; 0, Q) * cell volume(old) over the
 //                 2d modes (new grid, old grid)           filters.py:580-588, 653-679
 // Gaussian densities follow models.py:30-69: value = exp(log_norm - |L^-1 r|^2/2)
-// with L the lower Cholesky factor (computed on the host by numpy).
+// with L the lower Cholesky factor, solved as numpy.linalg.solve does it
+// (tri_quad in measure.cuh, from the dgetrf factors computed on the host).
 #pragma once
 #include "common.cuh"
 #include "tt.cuh"
@@ -24,7 +25,9 @@ struct EvalSpec {
   int n[MAXD];
   const double* axes[MAXD];   // coordinates of the black box's grid
   // Gaussian (prior, or process noise for the kernel): dim == d
-  double L[MAXD * MAXD];      // lower Cholesky, row-major
+  double LU[MAXD * MAXD];     // dgetrf factors of the lower Cholesky factor, row-major
+  int32_t piv[MAXD];
+  double inv[MAXD];
   double log_norm;
   double mean[MAXD];
   // likelihood
@@ -33,7 +36,9 @@ struct EvalSpec {
   int nang;
   int ang[MAXB];
   double z[MAXB];
-  double Lr[MAXB * MAXB];
+  double LUr[MAXB * MAXB];
+  int32_t pivr[MAXB];
+  double invr[MAXB];
   double log_norm_r;
   double H[MAXB * MAXD];
   // kernel
@@ -55,7 +60,7 @@ HD double eval_point(const EvalSpec& s, const int32_t* idx) {
   switch (s.kind) {
     case EV_GAUSS: {
       for (int k = 0; k < d; ++k) x[k] = s.axes[k][idx[k]] - s.mean[k];
-      return exp(s.log_norm - 0.5 * tri_quad(s.L, d, MAXD, x));
+      return exp(s.log_norm - 0.5 * tri_quad(SolveLU{s.LU, s.piv, s.inv, MAXD}, d, x));
     }
     case EV_LIKELIHOOD: {
       for (int k = 0; k < d; ++k) x[k] = s.axes[k][idx[k]];
@@ -66,7 +71,7 @@ HD double eval_point(const EvalSpec& s, const int32_t* idx) {
         const int a = s.ang[t];
         hz[a] = 180.0 - np_mod360(180.0 - hz[a]);
       }
-      return exp(s.log_norm_r - 0.5 * tri_quad(s.Lr, s.b, MAXB, hz));
+      return exp(s.log_norm_r - 0.5 * tri_quad(SolveLU{s.LUr, s.pivr, s.invr, MAXB}, s.b, hz));
     }
     case EV_KERNEL: {
       double disp[MAXD], q[MAXD];
@@ -80,7 +85,7 @@ HD double eval_point(const EvalSpec& s, const int32_t* idx) {
         for (int j = 0; j < d; ++j) acc += disp[j] * s.F[i * MAXD + j];
         q[i] = acc;
       }
-      return exp(s.log_norm - 0.5 * tri_quad(s.L, d, MAXD, q)) * s.cellvol;
+      return exp(s.log_norm - 0.5 * tri_quad(SolveLU{s.LU, s.piv, s.inv, MAXD}, d, q)) * s.cellvol;
     }
     case EV_TRANSITION: {
       const int h = s.dhalf;
@@ -91,7 +96,7 @@ HD double eval_point(const EvalSpec& s, const int32_t* idx) {
         for (int j = 0; j < h; ++j) acc += xo[j] * s.F[i * MAXD + j];
         diff[i] = s.axes[i][idx[i]] - acc;
       }
-      return exp(s.log_norm - 0.5 * tri_quad(s.L, h, MAXD, diff)) * s.cellvol;
+      return exp(s.log_norm - 0.5 * tri_quad(SolveLU{s.LU, s.piv, s.inv, MAXD}, h, diff)) * s.cellvol;
     }
     default:
       return NAN;

@@ -168,6 +168,16 @@ def gauss_consts(cov):
     return chol, -0.5 * (cov.shape[0] * math.log(2.0 * math.pi) + log_det)
 
 
+def solve_factors(chol):
+    """The factors numpy.linalg.solve(chol, b) works with inside
+    GaussianDensity.logpdf (models.py:60-63): LAPACK dgetrf of the Cholesky
+    factor (row-major LU), 0-based sequential row swaps and the reciprocal
+    pivots the trsm kernels multiply by."""
+    from scipy.linalg import lu_factor
+    lu, piv = lu_factor(np.atleast_2d(np.asarray(chol, dtype=float)), check_finite=False)
+    return np.ascontiguousarray(lu), piv.astype(np.int32), 1.0 / np.diag(lu)
+
+
 def pcg64_state(seed: int) -> list[int]:
     """numpy default_rng(seed) PCG64 state as the six words of ttgbf_cross_cfg."""
     st = np.random.PCG64(seed).state

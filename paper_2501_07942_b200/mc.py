@@ -69,3 +69,31 @@ def gather_rmse(local, group=None, device=None):
     cnt = allrows[:, -1].sum()
     rmse = np.sqrt(allrows[:, :-1].sum(axis=0) / max(cnt, 1.0))
     return rmse, allrows
+
+
+def run_monte_carlo(spec, bank_cfg, x0_mean, x0_cov, total_runs: int, kf: int, steps: int,
+                    backend=None, group=None, device=None):
+    """Sharded Monte Carlo driver: this rank's block of the ``total_runs``
+    seeded trajectories (SeedSequence((2024, run, 0)), models.py:165-194)
+    runs as one FilterBank through ``steps`` persistent-kernel filter steps;
+    then one all-gather of the per-run error sums forms the RMSE
+    (bench.py:369-371 of the reference).  Returns (rmse, allrows, recs, runs).
+    """
+    import torch.distributed as dist
+    from paper_2501_07942_b200.bank import FilterBank
+    from paper_2501_07942_b200.configs import simulate
+    rank = dist.get_rank(group) if dist.is_available() and dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    runs = shard(total_runs, world, rank)
+    d = np.asarray(spec["F"]).shape[0]
+    sts, ms = [], []
+    for r in runs:
+        s, m = simulate(spec, x0_mean, x0_cov, kf, np.random.SeedSequence((2024, int(r), 0)))
+        sts.append(s)
+        ms.append(m)
+    states, meas = np.stack(sts), np.stack(ms)
+    bank = FilterBank(spec, bank_cfg, len(runs), backend=backend)
+    recs = bank.run(meas, steps, x0_mean, x0_cov)
+    local = run_error_sums(recs["mean"], states, recs["k"], recs["status"] == 0, d)
+    rmse, allrows = gather_rmse(local, group=group, device=device)
+    return rmse, allrows, recs, runs

@@ -328,10 +328,14 @@ def sample_indices(shape):
     return np.stack([rng.integers(0, n, SAMPLE_COUNT) for n in shape], axis=1)
 
 
-def _perturbed_cross(seed):
+def _perturbed_cross(seed, scaled=False):
     """greedy_cross whose black box returns v * (1 + s * 2**-52), s in {-1, 0, 1}
     a deterministic hash of the multi-index: the
-    reference's own sensitivity to one-ulp evaluator differences."""
+    reference's own sensitivity to one-ulp evaluator differences.  scaled=True
+    uses v * (1 + s * 2**-52 * max(1, |log v|)) instead: the values are
+    exp(log-density), so a one-ulp difference in the log-density (what any
+    independent evaluation of the same formula has) is a relative error of
+    ulp(log v) ~ 2**-52 |log v| in v."""
     stock = rta.greedy_cross
     w = np.array([1000003, 10007, 101, 7919, 31, 13, 3, 17, 5, 29, 7, 11, 19, 23, 37, 41], dtype=np.int64)
 
@@ -342,26 +346,88 @@ def _perturbed_cross(seed):
             idx = np.asarray(idx, dtype=np.int64)
             v = np.asarray(inner(idx), dtype=float)
             s = ((idx @ w[: idx.shape[1]] + seed) % 3) - 1
+            if scaled:
+                with np.errstate(divide="ignore"):
+                    amp = np.maximum(1.0, np.abs(np.log(np.abs(v))))
+                amp[~np.isfinite(amp)] = 1.0
+                return v * (1.0 + s * 2.0 ** -52 * amp)
             return v * (1.0 + s * 2.0 ** -52)
 
         return stock(rta.BlackBoxTensor(shape=bb.shape, evaluate_many=ev), cfg)
     return wrapped
 
 
+class _NoisyNumpy:
+    """numpy with every einsum result moved by one ulp in a direction hashed
+    from its bits: stands in for a different summation order in the cross's
+    interpolant dot products (tt_algorithms.py:380-382, tensor_train.py:129-158)."""
+
+    def __init__(self, seed):
+        self._seed = seed
+
+    def __getattr__(self, name):
+        return getattr(np, name)
+
+    def einsum(self, *a, **k):
+        out = np.einsum(*a, **k)
+        if not isinstance(out, np.ndarray) or out.dtype != np.float64:
+            return out
+        bits = out.view(np.uint64)
+        s = ((bits * np.uint64(0x9E3779B97F4A7C15) + np.uint64(self._seed)) >> np.uint64(61)) % np.uint64(3)
+        s = s.astype(np.int64) - 1
+        return np.where(s > 0, np.nextafter(out, np.inf), np.where(s < 0, np.nextafter(out, -np.inf), out))
+
+
 def baseline_band():
-    """The same runs as baseline() with ulp-perturbed evaluators (two hash
-    seeds): tests/golden/baseline_band.npz.  |perturbed - baseline| per
+    """The same runs as baseline() with perturbed arithmetic: p1, p2 black-box
+    values moved by one ulp (two hash seeds), p3, p4 by one ulp of the
+    log-density, p5, p6 the cross's einsum results (interpolant dot products)
+    by one ulp: tests/golden/baseline_band.npz.  |perturbed - baseline| per
     (run, step) is the reference's self-disagreement band (Appendix A.3)."""
     stock_f, stock_a = rf.greedy_cross, rta.greedy_cross
-    out = {}
+    parts = {}
     try:
-        for seed in (1, 2):
-            rf.greedy_cross = _perturbed_cross(seed)
+        for seed, scaled in ((1, False), (2, False), (3, True), (4, True)):
+            rf.greedy_cross = _perturbed_cross(seed, scaled)
             part = baseline(write=False)
-            out.update({f"p{seed}/{k}": v for k, v in part.items()})
+            parts.update({f"p{seed}/{k}": v for k, v in part.items()})
+        rf.greedy_cross = stock_f
+        for seed in (5, 6):
+            rta.np = _NoisyNumpy(seed)
+            try:
+                part = baseline(write=False)
+            finally:
+                rta.np = np
+            parts.update({f"p{seed}/{k}": v for k, v in part.items()})
     finally:
         rf.greedy_cross, rta.greedy_cross = stock_f, stock_a
-    np.savez_compressed(os.path.join(HERE, "baseline_band.npz"), **out)
+    np.savez_compressed(os.path.join(HERE, "baseline_band.npz"), **summarize_band(parts))
+
+
+PERTURBATIONS = (1, 2, 3, 4, 5, 6)
+
+
+def summarize_band(parts):
+    """Compact band file: per config/run the perturbed runs' completed-step
+    counts (p1..p4/done) and per (run, step) the max relative difference of
+    the filtered mean, covariance and density sample from baseline.npz."""
+    z = np.load(os.path.join(HERE, "baseline.npz"))
+
+    def rel(a, b):
+        return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+    out = {}
+    for name in BASELINE_RUNS:
+        runs, steps = int(z[f"{name}/runs"]), int(z[f"{name}/steps"])
+        for r in range(runs):
+            for p in PERTURBATIONS:
+                out[f"p{p}/{name}/{r}/done"] = parts[f"p{p}/{name}/{r}/done"]
+                for k in range(steps):
+                    sk, pk = f"{name}/{r}/{k}", f"p{p}/{name}/{r}/{k}"
+                    if f"{sk}/sample" in z.files and f"{pk}/sample" in parts:
+                        out[f"{pk}/rel"] = np.array([rel(parts[f"{pk}/filt_mean"], z[f"{sk}/filt_mean"]),
+                                                     rel(parts[f"{pk}/filt_cov"], z[f"{sk}/filt_cov"]),
+                                                     rel(parts[f"{pk}/sample"], z[f"{sk}/sample"])])
+    return out
 
 
 def baseline(write=True):

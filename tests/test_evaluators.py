@@ -17,6 +17,10 @@ from paper_2501_07942_b200.configs import SPECS
 from scenario_util import rel, use_backend
 
 TOL = 1e-13
+# likelihood / kernel values are exp(log-density): one ulp of the log-density
+# (the solve and the transcendental functions round differently from numpy's
+# LAPACK / SVML code) moves the value by 2**-52 |log v|, up to ~1e-13 here
+TOL_EXP = 1e-12
 
 
 def kernel_grid(z, name, d):
@@ -29,9 +33,9 @@ def check_models(golden):
     for name, spec in SPECS.items():
         d = spec["F"].shape[0]
         lik = ev.likelihood_at_points(spec, z[f"{name}/z"], z[f"{name}/x"])
-        assert rel(lik, z[f"{name}/lik"]) <= TOL, (name, "likelihood", rel(lik, z[f"{name}/lik"]))
+        assert rel(lik, z[f"{name}/lik"]) <= TOL_EXP, (name, "likelihood", rel(lik, z[f"{name}/lik"]))
         kern = ev.kernel_values(spec, kernel_grid(z, name, d), z[f"{name}/kidx"])
-        assert rel(kern, z[f"{name}/kern"]) <= TOL, (name, "kernel", rel(kern, z[f"{name}/kern"]))
+        assert rel(kern, z[f"{name}/kern"]) <= TOL_EXP, (name, "kernel", rel(kern, z[f"{name}/kern"]))
 
 
 def check_prior_realign():

@@ -89,7 +89,7 @@ def test_persistent_run_overflow_gpu(golden, cuda, name):
     Hadamard rounding makes the step redo that stage in a borrowed buffer
     (spin-locked pool, both classes); the result must be the in-slot result."""
     from scenario_util import check_run, compare_scenario_run
-    rows_small = compare_scenario_run(golden, name, cuda, ws_bytes=24 << 20, big_slots=1, big_bytes=256 << 20,
+    rows_small = compare_scenario_run(golden, name, cuda, ws_bytes=64 << 20, big_slots=1, big_bytes=256 << 20,
                                       big2_slots=1, big2_bytes=512 << 20)
     check_run(rows_small)
     rows = compare_scenario_run(golden, name, cuda)

@@ -95,24 +95,29 @@ def test_stage_parity_injected(cuda, name):
     assert sample_rel(fin.numpy_cores(), out) <= 1e-7
 
 
-@pytest.mark.parametrize("name,filters,steps", [("C1", 4, 4), ("C2", 2, 2), ("C3", 4, 2), ("C4", 2, 1)])
-def test_baseline_configs_run(cuda, name, filters, steps):
-    """Persistent kernel on every BASELINE config: statuses are valid and every
-    completed step returns finite moments (tier 4: invariants only)."""
+@pytest.mark.parametrize("name,runs,steps", [("C1", (0, 1, 2, 5), 4), ("C2", (0, 1), 2), ("C3", (1, 6), 2),
+                                             ("C4", (2, 6), 1)])
+def test_baseline_configs_run(cuda, name, runs, steps):
+    """Persistent kernel on every BASELINE config, on trajectories whose first
+    step the reference completes (tests/golden/baseline.npz): at least one
+    completed step per config, only DegenerateDensityError as a failure
+    status, finite means and positive-definite covariances."""
+    from paper_2501_07942_b200 import _abi
     from paper_2501_07942_b200.bank import BankConfig, FilterBank
     cfg = BASELINE_CONFIGS[name]
     g, x = cfg["grid"], cfg["cross"]
     bc = BankConfig(n_per_axis=g["n_per_axis"], sigma_mult=g["sigma_mult"], round_tol=g["round_tol"],
                     round_max_rank=g["round_max_rank"], tol=x["tol"], max_rank=x["max_rank"], rng_seed=x["rng_seed"],
                     ws_bytes=1 << 30, state_doubles=1 << 20, cache_cap=1 << 21)
-    bank = FilterBank(cfg["spec"], bc, filters, backend=cuda)
+    bank = FilterBank(cfg["spec"], bc, len(runs), backend=cuda)
     Z = np.stack([simulate(cfg["spec"], cfg["x0_mean"], cfg["x0_cov"], cfg["steps"],
-                           np.random.SeedSequence((2024, r, 0)))[1] for r in range(filters)])
+                           np.random.SeedSequence((2024, r, 0)))[1] for r in runs])
     recs = bank.run(Z, steps, cfg["x0_mean"], cfg["x0_cov"])
     st = recs["status"]
-    assert set(np.unique(st)).issubset({-1, 0, 2, 3, 4, 5}), st
+    assert set(np.unique(st)).issubset({0, 3}), st
     d = cfg["spec"]["F"].shape[0]
     ok = st == 0
+    assert ok.sum() >= 1, st
     assert np.all(np.isfinite(recs["mean"][ok][:, :d]))
-    assert np.all(recs["cov_diag"][ok][:, :d] > 0)
-    assert not np.any(st == 4), "workspace exhausted"
+    covs = _abi.rec_cov(recs[ok], d)
+    assert np.all(np.linalg.eigvalsh(covs) > 0)

@@ -65,3 +65,53 @@ def test_gather_rmse_gloo_world2():
     for r in res:
         assert np.allclose(np.array(r[2]), ref)
         assert np.allclose(r[1], ref_rmse)
+
+
+def _bank_worker(rank, world, port, total, q):
+    """One rank of the sharded Monte Carlo driver over the engine's host
+    emulation (FilterBank.run), gloo all-gather of the error sums."""
+    import sys
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    from hostsim import HostBackend
+    from paper_2501_07942_b200.configs import SCENARIOS
+    from paper_2501_07942_b200.mc import run_monte_carlo
+    from scenario_util import bank_config
+    sc = SCENARIOS["radar_deg"]
+    rmse, allrows, recs, runs = run_monte_carlo(sc["spec"], bank_config(sc, ws_bytes=64 << 20), sc["x0_mean"],
+                                                sc["x0_cov"], total, sc["steps"], 3, backend=HostBackend())
+    q.put((rank, rmse.tolist(), allrows.tolist(), runs.tolist(), recs["status"].tolist()))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _run_ranks(world, total):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bank_worker, args=(r, world, port, total, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+def test_filterbank_run_sharded_gloo_world2():
+    """2 gloo ranks running FilterBank.run on their shards reproduce the
+    1-rank run: same per-run error rows, same RMSE, bit for bit."""
+    total = 5
+    one = _run_ranks(1, total)[0]
+    two = _run_ranks(2, total)
+    assert two[0][3] + two[1][3] == list(range(total))
+    for r in two:
+        assert np.array_equal(np.array(r[2]), np.array(one[2]))
+        assert r[1] == one[1]
+    assert np.all(np.isfinite(one[1])) and np.array(one[2])[:, -1].sum() > 0
