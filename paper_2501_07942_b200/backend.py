@@ -35,6 +35,7 @@ class CudaBackend:
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.stream = torch.cuda.current_stream(self.device)
+        self.nvtx = torch.cuda.nvtx
 
     @property
     def stream_ptr(self) -> int:

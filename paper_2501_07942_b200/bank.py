@@ -206,7 +206,14 @@ class FilterBank:
         if self.timeline is not None and hasattr(self.be, "event"):
             ev = (self.be.event(), self.be.event())
             ev[0].record(self.be.stream)
-        rc = fn(*args)
+        nvtx = getattr(self.be, "nvtx", None)
+        if nvtx is not None:
+            nvtx.range_push(f"{name} x{self.count}")   # ranges for nsys / ncu --nvtx
+        try:
+            rc = fn(*args)
+        finally:
+            if nvtx is not None:
+                nvtx.range_pop()
         if ev is not None:
             ev[1].record(self.be.stream)
             self.timeline.append((name, ev[0], ev[1]))

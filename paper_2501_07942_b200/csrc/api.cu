@@ -441,3 +441,16 @@ extern "C" int ttgbf_test_qr_apply(double* A, int m, int n, double* X, int nc, v
   return apply_q(c, ar, A, m, m, k, Ts.data(), false, X, m, nc, smem.data() + SMEM_RED + SMEM_XBLK);
 }
 #endif
+
+#ifdef ENGINE_HOSTSIM
+// Test-only: the cross's core solve lstsq(A, B) (gelsy emulation) for an r x r
+// A and r x nrhs B, both col-major; X r x nrhs col-major; *rank the rank used.
+extern "C" int ttgbf_test_lstsq(const double* A, const double* B, int r, int nrhs, double* X, int* rank) {
+  std::vector<double> smem(SMEM_DOUBLES);
+  const Ctx c = make_ctx(smem.data(), 0, 1);
+  std::vector<double> W((size_t)r * r), W2((size_t)r * r), tau(r), tau2(r), cn(r + 1);
+  std::vector<int> jpvt(r);
+  return lstsq_pivoted(c, A, 1, r, r, B, r, nrhs, X, r, W.data(), W2.data(), tau.data(), tau2.data(), jpvt.data(),
+                       cn.data(), rank);
+}
+#endif

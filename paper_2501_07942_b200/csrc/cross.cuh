@@ -199,12 +199,21 @@ HDN int x_solve_core(const Ctx& c, Arena& ar, XState& s, int k, double* sm) {
   ALLOC(W2, double, (int64_t)r * r, ar);
   ALLOC(tau, double, r, ar);
   ALLOC(tau2, double, r, ar);
-  ALLOC(cn, double, r, ar);
+  ALLOC(cn, double, r + 1, ar);
   ALLOC(jpvt, int, r, ar);
   // A_ls = ahat^T: (i,j) -> ahat[j][i]; B(i, row) = fib[row*cc + i]
   (void)sm;
+  int rank_used = 0;
   CK(lstsq_pivoted(c, s.ahat[k + 1], 1, s.maxr, r, s.fib[k], cc, A * n, s.core[k], cc, W, W2, tau, tau2, jpvt,
-                   cn, nullptr));
+                   cn, &rank_used));
+#if defined(ENGINE_HOSTSIM) && defined(ENGINE_TRACE)
+  {
+    double cs = 0.0;
+    for (int64_t e = 0; e < (int64_t)A * n; ++e)
+      for (int i = 0; i < r; ++i) cs += fabs(s.core[k][e * cc + i]);
+    fprintf(stderr, "SOLVE k=%d r=%d rank=%d rows=%d sum=%.17g\n", k, r, rank_used, A * n, cs);
+  }
+#endif
   ar.release(mk);
   return OK;
 }
@@ -410,6 +419,10 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
   c.sync();
   CK(x_errors(c, ar, C, spec, s, g, br, bc, 1, e, sm));
   if (c.leader()) cand[0] = Cand{rbest, cbest, e[0]};
+#if defined(ENGINE_HOSTSIM) && defined(ENGINE_TRACE)
+  fprintf(stderr, "HUNT b=%d rook=(%lld,%lld) e=%.17g seen=%.17g top=(%lld,%lld,%.17g)\n", b, (long long)rbest,
+          (long long)cbest, e[0], seen, (long long)cand[1].row, (long long)cand[1].col, cand[1].err);
+#endif
   c.sync();
   *ncand = nc_ + 1;
   *err_seen = seen;

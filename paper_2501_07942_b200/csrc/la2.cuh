@@ -504,6 +504,88 @@ HDN void qr_panel_nb(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
   }
 }
 
+// Left-looking form of qr_panel_nb (same reflectors, T and R up to
+// rounding): column j of the panel is brought up to date by the panel's
+// earlier reflectors only when it is reached -- w = V^T a_j, a_j -= V T^T w --
+// and reflected in the same sweep that writes it (its norm and the dots with
+// V for T accumulate while the updated values are stored).  Per column two
+// sweeps over the j earlier reflector columns plus one scaling sweep,
+// instead of the right-looking form's sweeps over every later column of the
+// panel: ~2j + 5 column passes instead of j + 5 + 3 (jb - j - 1).
+HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb, double* tau, double* T,
+                     double* sm) {
+  double* red = sm;        // >= NB + 1 reduction outputs
+  double* u = sm + 2 * NB; // T^T w (NB)
+  for (int jj = 0; jj < jb; ++jj) {
+    const int j = j0 + jj;
+    double* col = A + (int64_t)j * lda;
+    if (jj > 0) {
+      // pass A: w_q = V_q^T a_j, V_q = e_{j0+q} + A_q[r > j0+q]
+      double w[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) w[q] = 0.0;
+      for (int64_t r = j0 + 1 + c.tid; r < m; r += c.nt) {
+        const double x = col[r];
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          if (q < jj && r > j0 + q) w[q] = fma(A[(int64_t)(j0 + q) * lda + r], x, w[q]);
+      }
+      block_reduce_vec(c, w, jj, red);
+      // u = T^T (w + diagonal terms): u_p = sum_{q <= p} T(q, p) w_q
+      for (int p = c.tid; p < jj; p += c.nt) {
+        double acc = 0.0;
+        for (int q = 0; q <= p; ++q) acc += T[q + p * NB] * (red[q] + col[j0 + q]);
+        u[p] = acc;
+      }
+      c.sync();
+    }
+    // pass B: a_j -= V u (rows >= j0); norm^2 and V^T a_j below row j
+    double v[NB + 1];
+#pragma unroll
+    for (int q = 0; q <= NB; ++q) v[q] = 0.0;
+    for (int64_t r = j0 + c.tid; r < m; r += c.nt) {
+      double x = col[r];
+      if (jj > 0) {
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          if (q < jj) {
+            const int64_t dq = j0 + q;
+            if (r == dq) x -= u[q];
+            else if (r > dq) x = fma(-A[dq * lda + r], u[q], x);
+          }
+        col[r] = x;
+      }
+      if (r > j) {
+        v[0] = fma(x, x, v[0]);
+#pragma unroll
+        for (int q = 0; q < NB; ++q)
+          if (q < jj) v[1 + q] = fma(A[(int64_t)(j0 + q) * lda + r], x, v[1 + q]);
+      }
+    }
+    block_reduce_vec(c, v, jj + 1, red);
+    const double alpha = col[j];
+    double t, beta, scal;
+    larfg(alpha, sqrt(red[0]), &t, &beta, &scal);
+    for (int p = c.tid; p < NB; p += c.nt) {
+      double tv;
+      if (p < jj) {
+        double s = 0.0;
+        for (int q = p; q < jj; ++q) s += T[p + q * NB] * (A[(int64_t)(j0 + q) * lda + j] + scal * red[1 + q]);
+        tv = -t * s;
+      } else {
+        tv = p == jj ? t : 0.0;
+      }
+      T[p + jj * NB] = tv;
+    }
+    if (c.leader()) tau[j] = t;
+    // pass C: scale the reflector
+    for (int64_t r = j + 1 + c.tid; r < m; r += c.nt) col[r] *= scal;
+    c.sync();
+    if (c.leader()) col[j] = beta;
+    c.sync();
+  }
+}
+
 // Dense copy of the panel's reflectors V (rows j0..m-1, unit diagonal,
 // zeros above) into Vc (col-major, ld = m - j0).
 HD void copy_v(const Ctx& c, const double* A, int64_t lda, int m, int j0, int jb, double* Vc) {
@@ -590,6 +672,16 @@ HD void t_from_gram(const Ctx& c, const double* G, int jb, const double* tau, do
 // panel's T comes from one Gram GEMM of its explicit V (which the trailing
 // update needs anyway).
 constexpr int NS = 8;
+#ifndef TTGBF_QR_PANEL_LL
+#define TTGBF_QR_PANEL_LL 1
+#endif
+HDN void qr_panel_blk(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb, double* tau, double* T, double* sm) {
+#if TTGBF_QR_PANEL_LL
+  qr_panel_ll(c, A, lda, m, j0, jb, tau, T, sm);
+#else
+  qr_panel_nb(c, A, lda, m, j0, jb, tau, T, sm);
+#endif
+}
 #ifndef TTGBF_QR2_MIN_ROWS
 #define TTGBF_QR2_MIN_ROWS 2048
 #endif
@@ -604,7 +696,7 @@ HDN int geqrf_nb(const Ctx& c, Arena& ar, double* A, int64_t lda, int m, int n, 
     size_t mk = ar.mark();
     if (mr <= QR2_MIN_ROWS || jb <= NS) {
       PROF(c, 16);
-      qr_panel_nb(c, A, lda, m, j0, jb, tau, T, sm);
+      qr_panel_blk(c, A, lda, m, j0, jb, tau, T, sm);
     } else {
       PROF(c, 16);
       double *Ts_, *Vs;
@@ -612,7 +704,7 @@ HDN int geqrf_nb(const Ctx& c, Arena& ar, double* A, int64_t lda, int m, int n, 
       ALLOC(Vs, double, mr * NS, ar);
       for (int s0 = 0; s0 < jb; s0 += NS) {
         const int sb = imin(NS, jb - s0);
-        qr_panel_nb(c, A, lda, m, j0 + s0, sb, tau, Ts_, sm);
+        qr_panel_blk(c, A, lda, m, j0 + s0, sb, tau, Ts_, sm);
         if (s0 + sb < jb) {
           copy_v(c, A, lda, m, j0 + s0, sb, Vs);
           CK(apply_block(c, ar, Vs, m, j0 + s0, sb, Ts_, true, A + (int64_t)(j0 + s0 + sb) * lda, lda,

@@ -113,6 +113,79 @@ HD void larfg(double alpha, double xnorm, double* tau, double* beta, double* sca
   *beta = b;
 }
 
+// ---------------------------------------------------------------------------
+// LAPACK-faithful pieces of the cross's core solve (dgelsy -> dgeqp3/dlaqp2,
+// dlarfg, dlapy2, dnrm2).  The cross black boxes span 300 decades (kernel and
+// likelihood tails), so squared norms underflow where LAPACK's do not:
+// dnrm2 (OpenBLAS x86-64: an x87 extended-precision sum of squares) is
+// emulated by a power-of-two-scaled double-double sum; dlarfg rescales tiny
+// reflectors by 1/safmin like LAPACK; dgelsy scales A and B into
+// [smlnum, bignum] first.  Serial (one thread) -- r <= 160.
+// ---------------------------------------------------------------------------
+constexpr double LA_SAFMIN = 2.2250738585072014e-308;   // dlamch('S')
+constexpr double LA_EPS = 1.1102230246251565e-16;       // dlamch('E') = 2^-53
+constexpr double LA_PREC = 2.220446049250313e-16;       // dlamch('P') = eps * base
+
+HD double nrm2_ser(int n, const double* x, int64_t incx) {
+  double amax = 0.0;
+  for (int i = 0; i < n; ++i) amax = fmax(amax, fabs(x[i * incx]));
+  if (amax == 0.0 || !isfinite(amax)) return amax;
+  int e;
+  frexp(amax, &e);
+  const double sc = ldexp(1.0, -e), inv = ldexp(1.0, e);   // exact power-of-two scaling
+  double hi = 0.0, lo = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double v = x[i * incx] * sc;
+    const double p = v * v, pe = fma(v, v, -p);
+    const double t = hi + p;                             // two-sum
+    const double bp = t - hi;
+    const double err = (hi - (t - bp)) + (p - bp);
+    hi = t;
+    lo += err + pe;
+  }
+  const double sh = hi + lo, sl = lo - (sh - hi);
+  double r = sqrt(sh);
+  r = r + (fma(-r, r, sh) + sl) / (2.0 * r);             // one Newton step on the double-double sum
+  return r * inv;
+}
+
+HD double lapy2(double x, double y) {   // LAPACK dlapy2
+  const double xa = fabs(x), ya = fabs(y);
+  const double w = fmax(xa, ya), z = fmin(xa, ya);
+  if (z == 0.0) return w;
+  const double q = z / w;
+  const double q2 = q * q;     // separate roundings (reference Fortran, no FMA)
+  volatile double one_q2 = 1.0 + q2;
+  return w * sqrt(one_q2);
+}
+
+// LAPACK dlarfg on alpha / x(0:n) (x scaled in place): tau, beta; x <- v.
+HD void larfg_lapack(int n, double* alpha, double* x, int64_t incx, double* tau) {
+  if (n <= 0) { *tau = 0.0; return; }
+  double xnorm = nrm2_ser(n, x, incx);
+  if (xnorm == 0.0) { *tau = 0.0; return; }
+  double a = *alpha;
+  double beta = -copysign(lapy2(a, xnorm), a);
+  const double safmin = LA_SAFMIN / LA_EPS;
+  int knt = 0;
+  if (fabs(beta) < safmin) {
+    const double rsafmn = 1.0 / safmin;
+    do {
+      ++knt;
+      for (int i = 0; i < n; ++i) x[i * incx] *= rsafmn;
+      beta *= rsafmn;
+      a *= rsafmn;
+    } while (fabs(beta) < safmin && knt < 20);
+    xnorm = nrm2_ser(n, x, incx);
+    beta = -copysign(lapy2(a, xnorm), a);
+  }
+  *tau = (beta - a) / beta;
+  const double sc = 1.0 / (a - beta);
+  for (int i = 0; i < n; ++i) x[i * incx] *= sc;
+  for (int j = 0; j < knt; ++j) beta *= safmin;
+  *alpha = beta;
+}
+
 // Unblocked QR of the panel A[j0:m, j0:j0+jb) (column-major, lda); writes
 // tau[j0..j0+jb).  Each column: norm via block reduction, then the reflector
 // is applied to the remaining panel columns with one fused reduction pass.
@@ -680,57 +753,64 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
 #if !ENGINE_DEVICE
     const int lane = 0;
 #endif
+    // dgelsy: scale A into [smlnum, bignum] (the solution is rescaled below)
+    if (lane == 0) {
+      double anrm = 0.0;
+      for (int64_t e = 0; e < (int64_t)r * r; ++e) anrm = fmax(anrm, fabs(W[e]));
+      const double smlnum = LA_SAFMIN / LA_PREC, bignum = 1.0 / smlnum;
+      double ascl = 1.0;
+      if (anrm > 0.0 && anrm < smlnum) ascl = smlnum / anrm;
+      else if (anrm > bignum) ascl = bignum / anrm;
+      if (ascl != 1.0)
+        for (int64_t e = 0; e < (int64_t)r * r; ++e) W[e] *= ascl;
+      cn[r] = ascl;   // (cn has r + 1 entries)
+    }
+    WSYNC();
+    // dgeqp3 / dlaqp2: partial column norms vn1 (cn) / vn2 (tau2), downdated
+    for (int q = lane; q < r; q += L) { cn[q] = nrm2_ser(r, W + (int64_t)q * r, 1); tau2[q] = cn[q]; }
+    WSYNC();
+    const double tol3z = sqrt(LA_EPS);
     for (int j = 0; j < r; ++j) {
-      // column norms of the trailing block (each column summed in order)
-      double bv = -1.0;
-      int bi = r;
-      for (int q = j + lane; q < r; q += L) {
-        double s2 = 0.0;
-        for (int i = j; i < r; ++i) s2 = fma(W[i + (int64_t)q * r], W[i + (int64_t)q * r], s2);
-        cn[q] = s2;
-        if (s2 > bv) { bv = s2; bi = q; }
-      }
-#if ENGINE_DEVICE
-      for (int o = 16; o > 0; o >>= 1) {   // first index of the max
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-      }
-#endif
-      const int best = bi;
-      if (best != j) {
-        for (int i = lane; i < r; i += L) {
-          const double t = W[i + (int64_t)j * r];
-          W[i + (int64_t)j * r] = W[i + (int64_t)best * r];
-          W[i + (int64_t)best * r] = t;
-        }
-        if (lane == 0) { const int t = jpvt[j]; jpvt[j] = jpvt[best]; jpvt[best] = t; }
-      }
-      WSYNC();
-      double* col = W + (int64_t)j * r;
-      double t2 = 0.0, beta = 0.0, scal = 0.0;
       if (lane == 0) {
-        double xn = 0.0;
-        for (int i = j + 1; i < r; ++i) xn = fma(col[i], col[i], xn);
-        larfg(col[j], sqrt(xn), &t2, &beta, &scal);
+        int best = j;
+        for (int q = j + 1; q < r; ++q)
+          if (fabs(cn[q]) > fabs(cn[best])) best = q;   // idamax: first max
+        if (best != j) {
+          for (int i = 0; i < r; ++i) {
+            const double t = W[i + (int64_t)j * r];
+            W[i + (int64_t)j * r] = W[i + (int64_t)best * r];
+            W[i + (int64_t)best * r] = t;
+          }
+          const int t = jpvt[j]; jpvt[j] = jpvt[best]; jpvt[best] = t;
+          cn[best] = cn[j];
+          tau2[best] = tau2[j];
+        }
+        double t2 = 0.0;
+        if (j < r - 1) larfg_lapack(r - j - 1, &W[j + (int64_t)j * r], W + j + 1 + (int64_t)j * r, 1, &t2);
+        tau[j] = t2;
       }
-#if ENGINE_DEVICE
-      t2 = __shfl_sync(0xffffffffu, t2, 0);
-      beta = __shfl_sync(0xffffffffu, beta, 0);
-      scal = __shfl_sync(0xffffffffu, scal, 0);
-#endif
-      for (int i = j + 1 + lane; i < r; i += L) col[i] *= scal;
       WSYNC();
-      if (lane == 0) { col[j] = beta; tau[j] = t2; }
-      WSYNC();
-      if (t2 != 0.0) {
-        for (int q = j + 1 + lane; q < r; q += L) {
-          double* cq = W + (int64_t)q * r;
+      const double* col = W + (int64_t)j * r;
+      const double t2 = tau[j];
+      for (int q = j + 1 + lane; q < r; q += L) {
+        double* cq = W + (int64_t)q * r;
+        if (t2 != 0.0) {   // dlarf: H C = C - tau v (v^T C), v = [1; col(j+1:)]
           double w = cq[j];
           for (int i = j + 1; i < r; ++i) w = fma(col[i], cq[i], w);
           w *= t2;
           cq[j] -= w;
           for (int i = j + 1; i < r; ++i) cq[i] -= w * col[i];
+        }
+        if (cn[q] != 0.0) {   // dlaqp2's norm downdate / recomputation
+          const double a = fabs(cq[j]) / cn[q];
+          const double temp = fmax(1.0 - a * a, 0.0);
+          const double ratio = cn[q] / tau2[q];
+          if (temp * ratio * ratio <= tol3z) {
+            cn[q] = j + 1 < r ? nrm2_ser(r - j - 1, cq + j + 1, 1) : 0.0;
+            tau2[q] = cn[q];
+          } else {
+            cn[q] *= sqrt(temp);
+          }
         }
       }
       WSYNC();
@@ -774,21 +854,13 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
       WSYNC();
       for (int j = 0; j < rank; ++j) {
         double* col = W2 + (int64_t)j * r;
-        double t2 = 0.0, beta = 0.0, scal = 0.0;
+        double t2 = 0.0;
         if (lane == 0) {
-          double xn = 0.0;
-          for (int i = j + 1; i < r; ++i) xn = fma(col[i], col[i], xn);
-          larfg(col[j], sqrt(xn), &t2, &beta, &scal);
+          if (j < r - 1) larfg_lapack(r - j - 1, &col[j], col + j + 1, 1, &t2);
+          tau2[j] = t2;
         }
-#if ENGINE_DEVICE
-        t2 = __shfl_sync(0xffffffffu, t2, 0);
-        beta = __shfl_sync(0xffffffffu, beta, 0);
-        scal = __shfl_sync(0xffffffffu, scal, 0);
-#endif
-        for (int i = j + 1 + lane; i < r; i += L) col[i] *= scal;
         WSYNC();
-        if (lane == 0) { col[j] = beta; tau2[j] = t2; }
-        WSYNC();
+        t2 = tau2[j];
         for (int q = j + 1 + lane; q < rank; q += L) {
           double* cq = W2 + (int64_t)q * r;
           double w = cq[j];
@@ -805,10 +877,21 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
   c.sync();
   const int rank = c.ired[0];
   if (rank_out) *rank_out = rank;
+  // dgelsy's scaling of B into [smlnum, bignum] (one factor for all of B)
+  double bpart = 0.0;
+  for (int64_t e = c.tid; e < (int64_t)r * nrhs; e += c.nt) bpart = fmax(bpart, fabs(B[(e % r) + (e / r) * ldb]));
+  const double bnrm = block_max(c, bpart);
+  double bscl = 1.0;
+  {
+    const double smlnum = LA_SAFMIN / LA_PREC, bignum = 1.0 / smlnum;
+    if (bnrm > 0.0 && bnrm < smlnum) bscl = smlnum / bnrm;
+    else if (bnrm > bignum) bscl = bignum / bnrm;
+  }
+  const double xscl = cn[r] / bscl;   // X = (A-scale / B-scale) * solution of the scaled system
   // per right-hand side: y = Q^T b; triangular / min-norm solve; permute
   for (int q = c.tid; q < nrhs; q += c.nt) {
     double yy[X_MAXR_SOLVE], sol[X_MAXR_SOLVE];
-    for (int i = 0; i < r; ++i) yy[i] = B[i + (int64_t)q * ldb];
+    for (int i = 0; i < r; ++i) yy[i] = B[i + (int64_t)q * ldb] * bscl;
     for (int j = 0; j < r; ++j) {
       const double t2 = tau[j];
       if (t2 == 0.0) continue;
@@ -848,7 +931,7 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
         for (int i = j + 1; i < r; ++i) sol[i] -= w * v[i];
       }
     }
-    for (int i = 0; i < r; ++i) X[jpvt[i] + (int64_t)q * ldx] = sol[i];
+    for (int i = 0; i < r; ++i) X[jpvt[i] + (int64_t)q * ldx] = xscl == 1.0 ? sol[i] : sol[i] * xscl;
   }
   c.sync();
   return OK;

@@ -762,6 +762,53 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
 // the leading nw = min(want, p) vectors are formed (want = 0: all p):
 // U (m x nw, col-major), Vt (nw x n, row-major).
 // ---------------------------------------------------------------------------
+#if ENGINE_DEVICE
+// Pivoted-QR trailing update of svd_rrqr: apply the reflector (col, tau t) of
+// step j to columns j+1.. (NQ per warp) and recompute their norms below row j.
+template <int NQ>
+__device__ __forceinline__ void rrqr_update_cols(double* A, int m, int n, int j, const double* col, double t,
+                                                 double* cn, int warp, int nwarps, int lane) {
+  for (int q0 = j + 1 + warp * NQ; q0 < n; q0 += nwarps * NQ) {
+    double w[NQ];
+    double* cq[NQ];
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      w[u] = 0.0;
+      cq[u] = A + (int64_t)imin(q0 + u, n - 1) * m;
+    }
+    for (int r = j + lane; r < m; r += 32) {
+      const double v = r == j ? 1.0 : col[r];
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) w[u] = fma(v, cq[u][r], w[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      for (int o = 16; o > 0; o >>= 1) w[u] += __shfl_xor_sync(0xffffffffu, w[u], o);
+      w[u] *= t;
+    }
+    double nr[NQ];
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) nr[u] = 0.0;
+    for (int r = j + lane; r < m; r += 32) {
+      const double v = r == j ? 1.0 : col[r];
+#pragma unroll
+      for (int u = 0; u < NQ; ++u) {
+        if (q0 + u < n) {
+          const double x = cq[u][r] - w[u] * v;
+          cq[u][r] = x;
+          if (r > j) nr[u] = fma(x, x, nr[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+      for (int o = 16; o > 0; o >>= 1) nr[u] += __shfl_xor_sync(0xffffffffu, nr[u], o);
+      if (lane == 0 && q0 + u < n) cn[q0 + u] = nr[u];
+    }
+  }
+}
+#endif
+
 HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double eps_abs, double** U_out,
                  double** s_out, double** Vt_out, int* kk_out, double* sm, int want = 0) {
   PROF(c, 8);
@@ -845,21 +892,13 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
     c.sync();
     // apply to the trailing columns and refresh their norms (rows > j)
 #if ENGINE_DEVICE
-    for (int q = j + 1 + warp; q < n; q += nwarps) {
-      double* cq = A + (int64_t)q * m;
-      double w = 0.0;
-      for (int r = j + lane; r < m; r += 32) w = fma(r == j ? 1.0 : col[r], cq[r], w);
-      for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-      w *= t;
-      double nr = 0.0;
-      for (int r = j + lane; r < m; r += 32) {
-        const double v = cq[r] - w * (r == j ? 1.0 : col[r]);
-        cq[r] = v;
-        if (r > j) nr = fma(v, v, nr);
-      }
-      for (int o = 16; o > 0; o >>= 1) nr += __shfl_xor_sync(0xffffffffu, nr, o);
-      if (lane == 0) cn[q] = nr;
-    }
+    // several columns per warp when the trailing block is wide: more loads in
+    // flight per lane; every column keeps its own accumulation order, so the
+    // values are those of the one-column-per-warp loop
+    const int ntr = n - j - 1;
+    if (ntr >= 8 * nwarps) rrqr_update_cols<4>(A, m, n, j, col, t, cn, warp, nwarps, lane);
+    else if (ntr >= 2 * nwarps) rrqr_update_cols<2>(A, m, n, j, col, t, cn, warp, nwarps, lane);
+    else rrqr_update_cols<1>(A, m, n, j, col, t, cn, warp, nwarps, lane);
 #else
     for (int q = j + 1; q < n; ++q) {
       double* cq = A + (int64_t)q * m;

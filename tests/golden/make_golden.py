@@ -378,11 +378,41 @@ class _NoisyNumpy:
         return np.where(s > 0, np.nextafter(out, np.inf), np.where(s < 0, np.nextafter(out, -np.inf), out))
 
 
+class _NoisyScipy:
+    """scipy with linalg.lstsq solving a copy of A whose entries are moved by
+    one ulp in hashed directions: stands in for the roundoff differences of
+    any other pivoted-QR implementation of the cross's core solve
+    (tt_algorithms.py:305, gelsy)."""
+
+    def __init__(self, seed):
+        import scipy
+        self._scipy = scipy
+        self._seed = seed
+        outer = self
+
+        class _Linalg:
+            def __getattr__(self, name):
+                return getattr(scipy.linalg, name)
+
+            def lstsq(self, a, b, *args, **kw):
+                a = np.array(a, dtype=float, copy=True)
+                bits = a.view(np.uint64)
+                h = ((bits * np.uint64(0x9E3779B97F4A7C15) + np.uint64(outer._seed)) >> np.uint64(61)) % np.uint64(3)
+                h = h.astype(np.int64) - 1
+                a = np.where(h > 0, np.nextafter(a, np.inf), np.where(h < 0, np.nextafter(a, -np.inf), a))
+                return scipy.linalg.lstsq(a, b, *args, **kw)
+        self.linalg = _Linalg()
+
+    def __getattr__(self, name):
+        return getattr(self._scipy, name)
+
+
 def baseline_band():
     """The same runs as baseline() with perturbed arithmetic: p1, p2 black-box
     values moved by one ulp (two hash seeds), p3, p4 by one ulp of the
     log-density, p5, p6 the cross's einsum results (interpolant dot products)
-    by one ulp: tests/golden/baseline_band.npz.  |perturbed - baseline| per
+    by one ulp, p7, p8 the entries of the cross's core lstsq matrices by one
+    ulp: tests/golden/baseline_band.npz.  |perturbed - baseline| per
     (run, step) is the reference's self-disagreement band (Appendix A.3)."""
     stock_f, stock_a = rf.greedy_cross, rta.greedy_cross
     parts = {}
@@ -399,12 +429,20 @@ def baseline_band():
             finally:
                 rta.np = np
             parts.update({f"p{seed}/{k}": v for k, v in part.items()})
+        stock_sp = rta.scipy
+        for seed in (7, 8):
+            rta.scipy = _NoisyScipy(seed)
+            try:
+                part = baseline(write=False)
+            finally:
+                rta.scipy = stock_sp
+            parts.update({f"p{seed}/{k}": v for k, v in part.items()})
     finally:
         rf.greedy_cross, rta.greedy_cross = stock_f, stock_a
     np.savez_compressed(os.path.join(HERE, "baseline_band.npz"), **summarize_band(parts))
 
 
-PERTURBATIONS = (1, 2, 3, 4, 5, 6)
+PERTURBATIONS = (1, 2, 3, 4, 5, 6, 7, 8)
 
 
 def summarize_band(parts):

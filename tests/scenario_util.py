@@ -279,8 +279,9 @@ def check_baseline(rows):
 def reference_band(golden, cfg_name):
     """Per (run, step): the reference's own disagreement with itself when its
     black-box values are perturbed by one ulp (p1, p2) or one ulp of the
-    log-density (p3, p4), or its cross's einsum dot products by one ulp (p5,
-    p6) -- tests/golden/baseline_band.npz.  inf where a
+    log-density (p3, p4), its cross's einsum dot products by one ulp (p5, p6)
+    or the entries of its core-solve matrices by one ulp (p7, p8) --
+    tests/golden/baseline_band.npz.  inf where a
     perturbed run's failure step differs.  Returns {(run, step): band dict}."""
     z, b = golden("baseline"), golden("baseline_band")
     runs, steps = int(z[f"{cfg_name}/runs"]), int(z[f"{cfg_name}/steps"])
@@ -291,7 +292,7 @@ def reference_band(golden, cfg_name):
         for k in range(min(steps, done + 1)):
             sk = f"{cfg_name}/{r}/{k}"
             band = {"mean": 0.0, "cov": 0.0, "dens": 0.0}
-            for p in (1, 2, 3, 4, 5, 6):
+            for p in (1, 2, 3, 4, 5, 6, 7, 8):
                 pd = int(b[f"p{p}/{cfg_name}/{r}/done"])
                 if (k < done) != (k < pd) or unstable:
                     band = {key: np.inf for key in band}
