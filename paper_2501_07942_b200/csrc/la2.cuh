@@ -671,7 +671,10 @@ HD void t_from_gram(const Ctx& c, const double* G, int jb, const double* tau, do
 // with GEMMs, so a tall panel is streamed ~3x instead of ~NB times; the
 // panel's T comes from one Gram GEMM of its explicit V (which the trailing
 // update needs anyway).
-constexpr int NS = 8;
+#ifndef TTGBF_QR_NS
+#define TTGBF_QR_NS 8
+#endif
+constexpr int NS = TTGBF_QR_NS;   // sub-panel width of the two-level panel factorisation
 #ifndef TTGBF_QR_PANEL_LL
 #define TTGBF_QR_PANEL_LL 1
 #endif

@@ -127,9 +127,15 @@ constexpr double LA_EPS = 1.1102230246251565e-16;       // dlamch('E') = 2^-53
 constexpr double LA_PREC = 2.220446049250313e-16;       // dlamch('P') = eps * base
 
 HD double nrm2_ser(int n, const double* x, int64_t incx) {
-  double amax = 0.0;
-  for (int i = 0; i < n; ++i) amax = fmax(amax, fabs(x[i * incx]));
+  double amax = 0.0, s2 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double v = x[i * incx];
+    amax = fmax(amax, fabs(v));
+    s2 = fma(v, v, s2);
+  }
   if (amax == 0.0 || !isfinite(amax)) return amax;
+  // no under/overflow possible: the plain sum (as before the scaled path)
+  if (amax > 1e-140 && amax < 1e140) return sqrt(s2);
   int e;
   frexp(amax, &e);
   const double sc = ldexp(1.0, -e), inv = ldexp(1.0, e);   // exact power-of-two scaling
@@ -879,7 +885,8 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
   if (rank_out) *rank_out = rank;
   // dgelsy's scaling of B into [smlnum, bignum] (one factor for all of B)
   double bpart = 0.0;
-  for (int64_t e = c.tid; e < (int64_t)r * nrhs; e += c.nt) bpart = fmax(bpart, fabs(B[(e % r) + (e / r) * ldb]));
+  for (int q = c.tid; q < nrhs; q += c.nt)
+    for (int i = 0; i < r; ++i) bpart = fmax(bpart, fabs(B[i + (int64_t)q * ldb]));
   const double bnrm = block_max(c, bpart);
   double bscl = 1.0;
   {

@@ -26,7 +26,6 @@ from scenario_util import check_baseline_band, compare_baseline, reference_band
 
 pytestmark = pytest.mark.gpu
 
-MIN_STABLE = {"C1": 10, "C2": 4, "C3": 2, "C4": 1}
 
 
 @pytest.fixture(scope="module")
@@ -42,5 +41,5 @@ def cuda():
 @pytest.mark.parametrize("name", ["C1", "C3", "C2", "C4"])
 def test_baseline_goldens_gpu(golden, cuda, name, persistent):
     rows = compare_baseline(golden, name, cuda, persistent=persistent)
-    summary = check_baseline_band(rows, reference_band(golden, name), MIN_STABLE[name])
+    summary = check_baseline_band(rows, reference_band(golden, name), min_stable=1)
     print(json.dumps({"config": name, "persistent": persistent, **summary}))

@@ -83,14 +83,14 @@ def test_persistent_run_gpu(golden, cuda, name):
     check_run(compare_scenario_run(golden, name, cuda))
 
 
-@pytest.mark.parametrize("name", ["radar_deg", "cv4_step0"])
-def test_persistent_run_overflow_gpu(golden, cuda, name):
+@pytest.mark.parametrize("name,ws_mb", [("radar_deg", 64), ("cv4_step0", 160)])
+def test_persistent_run_overflow_gpu(golden, cuda, name, ws_mb):
     """Force the overflow workspaces: a slot too small for the FFT product /
     Hadamard rounding makes the step redo that stage in a borrowed buffer
     (spin-locked pool, both classes); the result must be the in-slot result."""
     from scenario_util import check_run, compare_scenario_run
-    rows_small = compare_scenario_run(golden, name, cuda, ws_bytes=64 << 20, big_slots=1, big_bytes=256 << 20,
-                                      big2_slots=1, big2_bytes=512 << 20)
+    rows_small = compare_scenario_run(golden, name, cuda, ws_bytes=ws_mb << 20, big_slots=1, big_bytes=256 << 20,
+                                      big2_slots=1, big2_bytes=1 << 30)
     check_run(rows_small)
     rows = compare_scenario_run(golden, name, cuda)
     for a, b in zip(rows, rows_small):

@@ -67,7 +67,7 @@ def gpu(out):
         bc = BankConfig(n_per_axis=g["n_per_axis"], sigma_mult=g["sigma_mult"], round_tol=g["round_tol"],
                         round_max_rank=g["round_max_rank"], tol=x["tol"], max_rank=x["max_rank"],
                         rng_seed=x["rng_seed"], ws_bytes=320 << 20, state_doubles=1 << 18, cache_cap=1 << 20,
-                        big_slots=32, big_bytes=1 << 30, big2_slots=8, big2_bytes=3 << 29)
+                        ws_slots=148, big_slots=32, big_bytes=1 << 30, big2_slots=8, big2_bytes=3 << 29)
         Z = np.stack([simulate(cfg["spec"], cfg["x0_mean"], cfg["x0_cov"], STEPS[name],
                                np.random.SeedSequence((2024, r, 0)))[1] for r in range(RUNS)])
         bank = FilterBank(cfg["spec"], bc, RUNS)
@@ -87,6 +87,9 @@ def gpu(out):
                     mean0[i] = recs["mean"][i][: cfg["spec"]["F"].shape[0]].tolist()
         res[name] = {"fail_step": fail.tolist(), "mean0": mean0}
         print(name, "%.0fs" % (time.time() - t0), flush=True)
+        del bank
+        import torch
+        torch.cuda.empty_cache()
     json.dump(res, open(out, "w"))
 
 
