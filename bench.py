@@ -309,6 +309,7 @@ def run_ours(args):
     kf = cfg["steps"]
     dev = torch.device("cuda", local)
     peak_fp64 = rl.measure_fp64_peak(torch, dev)
+    peak_fp64_sustained = rl.measure_fp64_sustained(torch, dev)
     bank = FilterBank(cfg["spec"], bcfg, B)
     stats = {"flops": 0.0, "cycles": np.zeros(8), "prof": np.zeros(32), "ranks": None}
 
@@ -418,6 +419,8 @@ def run_ours(args):
                      "hbm_achieved_gbs": (traffic_per_launch / dom_time / 1e9) if traffic_per_launch and dom_time else None,
                      "hbm_peak_gbs": hbm_peak,
                      "peak_source": "cuBLAS DGEMM 8192^3 burst measured in this run (MEASURED_PEAKS.json has no FP64)",
+                     "peak_sustained": peak_fp64_sustained,
+                     "frac_of_sustained": achieved / peak_fp64_sustained,
                      "algorithmic_flops_per_launch": flops_per_launch, "launch_s": dom_time},
         "kernel_time_s": {k: sum(v) for k, v in per_kernel.items()},
         "device_busy_frac": kern_total / dev_s if dev_s > 0 else None,

@@ -392,11 +392,10 @@ extern "C" int ttgbf_test_draws(int kind, uint64_t* state6, const int* shape, in
   g.has32 = (uint32_t)state6[4]; g.u32 = (uint32_t)state6[5];
   PcgJump jt;
   pcg_make_jump(g, &jt);
-  DrawBuf db;
   if (kind == 0) {
     std::vector<int64_t> tmp(K * d);
     std::vector<int32_t> o32(K * d);
-    warp_integers(c, &g, &jt, shape, d, K, o32.data(), tmp.data(), &db);
+    warp_integers(c, &g, &jt, shape, d, K, o32.data(), tmp.data());
     for (int64_t e = 0; e < K * d; ++e) out[e] = o32[e];
   } else {
     std::vector<int32_t> disp(pop + 16, -1);
@@ -404,7 +403,7 @@ extern "C" int ttgbf_test_draws(int kind, uint64_t* state6, const int* shape, in
     std::vector<uint8_t> flags(size + 16);
     std::vector<uint32_t> gset(4 * (size + 16) + 64);
     warp_choice(c, &g, &jt, pop, size, out, disp.data(), touch.data(), draws.data(), flags.data(),
-                reinterpret_cast<uint32_t*>(smem.data() + SMEM_RED + SMEM_XBLK), 2 * SMEM_SCRATCH_DOUBLES, gset.data(), &db);
+                reinterpret_cast<uint32_t*>(smem.data() + SMEM_RED + SMEM_XBLK), 2 * SMEM_SCRATCH_DOUBLES, gset.data());
     for (int64_t q = 0; q < pop; ++q)
       if (disp[q] != -1) return 99;   // displacement map must be restored
   }

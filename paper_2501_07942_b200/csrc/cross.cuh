@@ -57,7 +57,6 @@ struct XShared {           // leader-published scalars
   Pcg64 rng;
   int64_t i0, i1, i2;
   double f0, f1;
-  DrawBuf db;              // warp-parallel draw buffer
 };
 
 struct ChoiceWs {
@@ -335,8 +334,8 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
   ALLOC(e, double, X_SCAN, ar);
   {
     PROF(c, 10);
-    warp_choice(c, &sh->rng, rws.jt, g.nrow, qr, cr, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
-    warp_choice(c, &sh->rng, rws.jt, g.ncol, qc, cc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, g.nrow, qr, cr, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
+    warp_choice(c, &sh->rng, rws.jt, g.ncol, qc, cc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
   }
   if (c.leader()) {
     for (int i = 0; i < qr; ++i)
@@ -373,7 +372,7 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
     int nsr = 0;
     if (g.nrow > X_SCAN) {
       PROF(c, 10);
-      warp_choice(c, &sh->rng, rws.jt, g.nrow, X_SCAN, br, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
+      warp_choice(c, &sh->rng, rws.jt, g.nrow, X_SCAN, br, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
     }
     if (c.leader()) {
       if (g.nrow > X_SCAN) nsr = X_SCAN;
@@ -393,7 +392,7 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
     int nsc = 0;
     if (g.ncol > X_SCAN) {
       PROF(c, 10);
-      warp_choice(c, &sh->rng, rws.jt, g.ncol, X_SCAN, bc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
+      warp_choice(c, &sh->rng, rws.jt, g.ncol, X_SCAN, bc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
     }
     if (c.leader()) {
       if (g.ncol > X_SCAN) nsc = X_SCAN;
@@ -459,7 +458,7 @@ HDN int x_check(const Ctx& c, Arena& ar, Cache* C, XShared* sh, const ChoiceWs& 
   ALLOC(tv, double, K, ar);
   if (cnt > count) {
     PROF(c, 10);
-    warp_choice(c, &sh->rng, rws.jt, cnt, count, sel, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset, &sh->db);
+    warp_choice(c, &sh->rng, rws.jt, cnt, count, sel, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
   } else if (c.leader()) {
     for (int64_t i = 0; i < cnt; ++i) sel[i] = i;
   }
@@ -599,7 +598,7 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
   double* pv;
   ALLOC(probes, int32_t, K0 * d, ar);
   ALLOC(pv, double, K0, ar);
-  warp_integers(c, &sh->rng, rws.jt, spec.n, d, nprobe, probes, rws.draws, &sh->db);
+  warp_integers(c, &sh->rng, rws.jt, spec.n, d, nprobe, probes, rws.draws);
   for (int64_t e = c.tid; e < (int64_t)cfg.nseeds * d; e += c.nt) probes[(int64_t)nprobe * d + e] = cfg.seeds[e];
   c.sync();
   CK(cache_eval(c, ar, C, spec, probes, K0, pv, sm));
@@ -728,7 +727,7 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
       }
     }
     // fresh uniform probes
-    warp_integers(c, &sh->rng, rws.jt, spec.n, d, fresh, fp, rws.draws, &sh->db);
+    warp_integers(c, &sh->rng, rws.jt, spec.n, d, fresh, fp, rws.draws);
     c.sync();
     CK(cache_eval(c, ar, C, spec, fp, fresh, fv, sm));
     double thr = cfg.tol * fmax(C->max_abs, X_TINY);
@@ -787,7 +786,7 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
   ALLOC(vref, double, nv, ar);
   ALLOC(vt, double, nv, ar);
   if ((int64_t)nv * d > X_GATE + X_SCAN) return E_ARG;
-  warp_integers(c, &sh->rng, rws.jt, spec.n, d, nv, vp, rws.draws, &sh->db);
+  warp_integers(c, &sh->rng, rws.jt, spec.n, d, nv, vp, rws.draws);
   c.sync();
   CK(cache_eval(c, ar, C, spec, vp, nv, vref, sm));
   auto validate = [&](const TT& cand_tt, double* res) -> int {

@@ -512,8 +512,12 @@ HDN void qr_panel_nb(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
 // sweeps over the j earlier reflector columns plus one scaling sweep,
 // instead of the right-looking form's sweeps over every later column of the
 // panel: ~2j + 5 column passes instead of j + 5 + 3 (jb - j - 1).
+#ifndef TTGBF_QR_UNROLL
+#define TTGBF_QR_UNROLL 4
+#endif
 HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb, double* tau, double* T,
                      double* sm) {
+  constexpr int QU = TTGBF_QR_UNROLL;   // rows per thread per iteration
   double* red = sm;        // >= NB + 1 reduction outputs
   double* u = sm + 2 * NB; // T^T w (NB)
   for (int jj = 0; jj < jb; ++jj) {
@@ -524,11 +528,25 @@ HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
       double w[NB];
 #pragma unroll
       for (int q = 0; q < NB; ++q) w[q] = 0.0;
-      for (int64_t r = j0 + 1 + c.tid; r < m; r += c.nt) {
-        const double x = col[r];
+      // QU rows per iteration: their loads are independent, so each thread
+      // keeps QU x (jj + 1) loads in flight (the panel streams from L2/HBM)
+      for (int64_t r0 = j0 + 1 + c.tid; r0 < m; r0 += (int64_t)QU * c.nt) {
+        double x[QU];
+#pragma unroll
+        for (int u = 0; u < QU; ++u) {
+          const int64_t r = r0 + (int64_t)u * c.nt;
+          x[u] = r < m ? col[r] : 0.0;
+        }
 #pragma unroll
         for (int q = 0; q < NB; ++q)
-          if (q < jj && r > j0 + q) w[q] = fma(A[(int64_t)(j0 + q) * lda + r], x, w[q]);
+          if (q < jj) {
+            const double* aq = A + (int64_t)(j0 + q) * lda;
+#pragma unroll
+            for (int u = 0; u < QU; ++u) {
+              const int64_t r = r0 + (int64_t)u * c.nt;
+              if (r < m && r > j0 + q) w[q] = fma(aq[r], x[u], w[q]);
+            }
+          }
       }
       block_reduce_vec(c, w, jj, red);
       // u = T^T (w + diagonal terms): u_p = sum_{q <= p} T(q, p) w_q
@@ -543,23 +561,43 @@ HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
     double v[NB + 1];
 #pragma unroll
     for (int q = 0; q <= NB; ++q) v[q] = 0.0;
-    for (int64_t r = j0 + c.tid; r < m; r += c.nt) {
-      double x = col[r];
+    for (int64_t r0 = j0 + c.tid; r0 < m; r0 += (int64_t)QU * c.nt) {
+      double x[QU];
+#pragma unroll
+      for (int u2 = 0; u2 < QU; ++u2) {
+        const int64_t r = r0 + (int64_t)u2 * c.nt;
+        x[u2] = r < m ? col[r] : 0.0;
+      }
       if (jj > 0) {
 #pragma unroll
         for (int q = 0; q < NB; ++q)
           if (q < jj) {
             const int64_t dq = j0 + q;
-            if (r == dq) x -= u[q];
-            else if (r > dq) x = fma(-A[dq * lda + r], u[q], x);
-          }
-        col[r] = x;
-      }
-      if (r > j) {
-        v[0] = fma(x, x, v[0]);
+            const double* aq = A + dq * lda;
 #pragma unroll
-        for (int q = 0; q < NB; ++q)
-          if (q < jj) v[1 + q] = fma(A[(int64_t)(j0 + q) * lda + r], x, v[1 + q]);
+            for (int u2 = 0; u2 < QU; ++u2) {
+              const int64_t r = r0 + (int64_t)u2 * c.nt;
+              if (r < m) {
+                if (r == dq) x[u2] -= u[q];
+                else if (r > dq) x[u2] = fma(-aq[r], u[q], x[u2]);
+              }
+            }
+          }
+#pragma unroll
+        for (int u2 = 0; u2 < QU; ++u2) {
+          const int64_t r = r0 + (int64_t)u2 * c.nt;
+          if (r < m) col[r] = x[u2];
+        }
+      }
+#pragma unroll
+      for (int u2 = 0; u2 < QU; ++u2) {
+        const int64_t r = r0 + (int64_t)u2 * c.nt;
+        if (r < m && r > j) {
+          v[0] = fma(x[u2], x[u2], v[0]);
+#pragma unroll
+          for (int q = 0; q < NB; ++q)
+            if (q < jj) v[1 + q] = fma(A[(int64_t)(j0 + q) * lda + r], x[u2], v[1 + q]);
+        }
       }
     }
     block_reduce_vec(c, v, jj + 1, red);

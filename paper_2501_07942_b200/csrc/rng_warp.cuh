@@ -31,10 +31,6 @@ HD void pcg_make_jump(const Pcg64& g, PcgJump* j) {
   }
 }
 
-struct DrawBuf {          // (placeholder: draws are position-addressed, no buffer)
-  int unused;
-};
-
 #if ENGINE_DEVICE
 #define LANE_LOOP(l) for (int l = (c.tid & 31), _once = 0; _once < 1; ++_once)
 #else
@@ -112,9 +108,7 @@ HD void sp_seek(StreamPos& sp, const PcgJump* jt, int64_t p) {
 // stream value P + l; the first rejection or zero bound ends the accepted
 // run and is resolved uniformly).  g is left as numpy leaves it.
 template <class Bound>
-HDN void warp_draws(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t n, Bound bound, int64_t* out,
-                    DrawBuf* db) {
-  (void)db;
+HDN void warp_draws(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t n, Bound bound, int64_t* out) {
   const bool w0 = !ENGINE_DEVICE || c.tid < 32;
   if (w0 && n > 0) {
     StreamPos sp;
@@ -213,8 +207,8 @@ struct BoundDown {  // i = hi - t
 
 // rng.integers(0, shape, size=(K, d)) -> out32 (K*d), via an int64 scratch
 HDN void warp_integers(const Ctx& c, Pcg64* g, const PcgJump* jt, const int* shape, int d, int64_t K,
-                       int32_t* out32, int64_t* tmp, DrawBuf* db) {
-  warp_draws(c, g, jt, K * d, BoundCols{shape, d}, tmp, db);
+                       int32_t* out32, int64_t* tmp) {
+  warp_draws(c, g, jt, K * d, BoundCols{shape, d}, tmp);
   for (int64_t e = c.tid; e < K * d; e += c.nt) out32[e] = (int32_t)tmp[e];
   c.sync();
 }
@@ -292,12 +286,12 @@ HD void swap_resolve(const Ctx& c, int64_t ns, IFn I, JFn J, Get get, Set set, F
 // gset: global scratch >= 2*(gen_mask(1.2*size)+1) uint32.
 HDN void warp_choice(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t pop, int64_t size, int64_t* out,
                      int32_t* disp, int64_t* touch, int64_t* draws, uint8_t* flags, uint32_t* sset,
-                     int64_t sset_words32, uint32_t* gset, DrawBuf* db) {
+                     int64_t sset_words32, uint32_t* gset) {
   if (pop > 10000 && size > pop / 50) {
     int64_t first = pop - size;
     if (first < 1) first = 1;
     const int64_t ns = pop - first;
-    warp_draws(c, g, jt, ns, BoundDown{pop - 1}, draws, db);   // draw t: j for i = pop-1-t
+    warp_draws(c, g, jt, ns, BoundDown{pop - 1}, draws);   // draw t: j for i = pop-1-t
     const int64_t lo = pop - size;
     swap_resolve(
         c, ns, [=](int64_t t) { return pop - 1 - t; }, [=](int64_t t) { return draws[t]; },
@@ -313,9 +307,9 @@ HDN void warp_choice(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t pop, int
     return;
   }
   // Floyd: draws val_t for j_t = pop-size+t, then the shuffle draws (i = size-1..1)
-  warp_draws(c, g, jt, size, BoundUp{pop - size}, draws, db);
+  warp_draws(c, g, jt, size, BoundUp{pop - size}, draws);
   int64_t* sdraws = touch;
-  warp_draws(c, g, jt, size > 1 ? size - 1 : 0, BoundDown{size - 1}, sdraws, db);
+  warp_draws(c, g, jt, size > 1 ? size - 1 : 0, BoundDown{size - 1}, sdraws);
   // first occurrence of each value: open addressing, key = value, payload = min t
   const uint64_t mask = gen_mask((uint64_t)(1.2 * (double)size));
   const int64_t tsz = (int64_t)mask + 1;

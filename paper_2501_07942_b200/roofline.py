@@ -83,6 +83,32 @@ def step_flops(dm_row, dt_row, d, b, n):
     return fm, ft
 
 
+def measure_fp64_sustained(torch, device, n=8192, seconds=3.0):
+    """cuBLAS DGEMM back to back for ~`seconds` (CUDA events around the whole
+    sequence): the sustained FP64 rate, the fair denominator for a launch
+    that runs for tens of seconds (the burst figure is the best single GEMM)."""
+    a = torch.randn(n, n, dtype=torch.float64, device=device)
+    b = torch.randn(n, n, dtype=torch.float64, device=device)
+    c = torch.matmul(a, b)
+    torch.cuda.synchronize(device)
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    torch.matmul(a, b, out=c)
+    e.record()
+    torch.cuda.synchronize(device)
+    one = s.elapsed_time(e) / 1e3
+    reps = max(2, int(seconds / max(one, 1e-4)))
+    s.record()
+    for _ in range(reps):
+        torch.matmul(a, b, out=c)
+    e.record()
+    torch.cuda.synchronize(device)
+    t = s.elapsed_time(e) / 1e3
+    del a, b, c
+    return 2.0 * n ** 3 * reps / t / 1e12
+
+
 def measure_fp64_peak(torch, device, n=8192, reps=5):
     """cuBLAS DGEMM burst (best of reps) in TFLOP/s -- the FP64 roofline denominator."""
     a = torch.randn(n, n, dtype=torch.float64, device=device)

@@ -95,3 +95,27 @@ def test_persistent_run_overflow_gpu(golden, cuda, name, ws_mb):
     rows = compare_scenario_run(golden, name, cuda)
     for a, b in zip(rows, rows_small):
         assert a == b, (a, b)
+
+
+@pytest.mark.parametrize("ranks,n,cap", [((1, 90, 700, 120, 1), 21, 20), ((1, 200, 640, 300, 1), 17, None)])
+def test_round_wide_gpu(cuda, ranks, n, cap):
+    """Product-width rounding (the bench's FFT products reach rank ~700): the
+    truncated rank-revealing SVD (pivoted QR stopped at 1e-3 delta) against
+    the oracle's full numpy SVD rounding (tensor_train.py:327-360), with the
+    rank cap binding and with the tolerance deciding."""
+    from paper_2501_07942_b200 import tensor_train as G
+    from scenario_util import use_backend
+    use_backend(cuda)
+    rs = np.random.RandomState(sum(ranks))
+    cores = []
+    for k in range(len(ranks) - 1):
+        core = rs.randn(ranks[k], n, ranks[k + 1])
+        core *= (0.93 ** np.arange(ranks[k + 1]))[None, None, :]
+        cores.append(core)
+    ref = T.round_tt(cores, 1e-8, cap)
+    got = G.tt_round(G.TensorTrain.from_cores(cores), 1e-8, cap)
+    assert got.ranks == T.ranks_of(ref)
+    rng = np.random.default_rng(3)
+    idx = np.stack([rng.integers(0, n, 10_000) for _ in range(len(ranks) - 1)], axis=1)
+    a, b = T.at_indices(got.numpy_cores(), idx), T.at_indices(ref, idx)
+    assert np.max(np.abs(a - b)) <= 1e-9 * np.max(np.abs(b))
