@@ -99,7 +99,7 @@ HDN int cache_init(const Ctx& c, Arena& ar, Cache*& C, int d, const int* n, int6
   ALLOC(keys, Key, cap, ar);
   ALLOC(vals, double, cap, ar);
   ALLOC(table, int32_t, tsz, ar);
-  for (uint64_t i = c.tid; i < tsz; i += c.nt) table[i] = -1;
+  par_fill_i32(c, table, (int64_t)tsz, -1);
   if (c.leader()) {
     C->d = d;
     C->bits = bits;

@@ -253,8 +253,36 @@ HD Arena make_ws_arena(void* ws, int64_t ws_bytes, int item) {
 HD void par_fill(const Ctx& c, double* p, int64_t n, double v) {
   for (int64_t i = c.tid; i < n; i += c.nt) p[i] = v;
 }
+// Copy with 16-byte accesses where dst and src share their alignment (half
+// the load/store instructions of the element loop; same bytes written).
 HD void par_copy(const Ctx& c, double* dst, const double* src, int64_t n) {
+#if ENGINE_DEVICE
+  if ((((uintptr_t)dst ^ (uintptr_t)src) & 15) == 0) {
+    const int64_t head = (((uintptr_t)dst & 15) != 0) ? 1 : 0;
+    if (head && c.tid == 0 && n > 0) dst[0] = src[0];
+    const int64_t nv = (n - head) / 2;
+    double2* d2 = reinterpret_cast<double2*>(dst + head);
+    const double2* s2 = reinterpret_cast<const double2*>(src + head);
+    for (int64_t i = c.tid; i < nv; i += c.nt) d2[i] = s2[i];
+    for (int64_t i = head + 2 * nv + c.tid; i < n; i += c.nt) dst[i] = src[i];
+    return;
+  }
+#endif
   for (int64_t i = c.tid; i < n; i += c.nt) dst[i] = src[i];
+}
+// int32 fill with 16-byte stores (p 16-byte aligned -- arena allocations are).
+HD void par_fill_i32(const Ctx& c, int32_t* p, int64_t n, int32_t v) {
+#if ENGINE_DEVICE
+  if (((uintptr_t)p & 15) == 0) {
+    const int64_t nv = n / 4;
+    int4* p4 = reinterpret_cast<int4*>(p);
+    const int4 v4 = make_int4(v, v, v, v);
+    for (int64_t i = c.tid; i < nv; i += c.nt) p4[i] = v4;
+    for (int64_t i = 4 * nv + c.tid; i < n; i += c.nt) p[i] = v;
+    return;
+  }
+#endif
+  for (int64_t i = c.tid; i < n; i += c.nt) p[i] = v;
 }
 
 }  // namespace tg

@@ -347,25 +347,31 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
   int nc_ = 0;
   double seen = 0.0;
   int64_t rbest = 0, cbest = 0;
-  if (c.leader()) {
-    // argsort ascending (stable) then reversed: descending, later index first on ties
-    int ord[X_CAND * X_CAND];
-    for (int i = 0; i < nb; ++i) ord[i] = i;
-    for (int i = 1; i < nb; ++i) {
-      int p = ord[i], q = i - 1;
-      while (q >= 0 && e[ord[q]] > e[p]) { ord[q + 1] = ord[q]; --q; }
-      ord[q + 1] = p;
+  {
+    // argsort ascending (stable) then reversed: descending, later index first
+    // on ties.  Thread i places element i at its stable rank (the number of
+    // elements that precede it), all ranks in parallel.
+    double* es = sm;   // nb <= X_CAND^2 errors staged in SMEM
+    for (int i = c.tid; i < nb; i += c.nt) es[i] = e[i];
+    c.sync();
+    for (int i = c.tid; i < nb; i += c.nt) {
+      const double ei = es[i];
+      int rank = 0;
+      for (int j = 0; j < nb; ++j) {
+        const double ej = es[j];
+        rank += (ej < ei || (ej == ei && j < i)) ? 1 : 0;
+      }
+      cand[1 + (nb - 1 - rank)] = Cand{br[i], bc[i], ei};
     }
-    for (int i = 0; i < nb; ++i) {
-      const int j = ord[nb - 1 - i];
-      cand[1 + i] = Cand{br[j], bc[j], e[j]};
+    c.sync();
+    if (c.leader()) {
+      nc_ = nb;
+      if (nb > 0) { seen = cand[1].err; rbest = cand[1].row; cbest = cand[1].col; }
+      sh->i0 = rbest; sh->i1 = cbest; sh->f0 = seen;
     }
-    nc_ = nb;
-    if (nb > 0) { seen = cand[1].err; rbest = cand[1].row; cbest = cand[1].col; }
-    sh->i0 = rbest; sh->i1 = cbest; sh->f0 = seen;
   }
-  c.sync();
   rbest = sh->i0; cbest = sh->i1; seen = sh->f0;
+  nc_ = nb;
   c.sync();
   for (int it = 0; it < X_ROOK; ++it) {
     // column scan over (sampled) rows
@@ -573,7 +579,7 @@ HDN int greedy_cross(const Ctx& c, Arena& ar, const EvalSpec& spec, const CrossC
     ALLOC(jt, PcgJump, 1, ar);
     if (c.leader()) pcg_make_jump(cfg.rng, jt);
     rws.jt = jt;
-    for (int64_t q = c.tid; q < dcap; q += c.nt) rws.disp[q] = -1;
+    par_fill_i32(c, rws.disp, dcap, -1);
     c.sync();
   }
   if (d == 1) {

@@ -591,15 +591,25 @@ HDN int tt_hadamard(const Ctx& c, Arena& ar, const TT& A, const TT& B, TT& out) 
   CK(tt_alloc(ar, out, A.d, n, r));
   for (int k = 0; k < A.d; ++k) {
     const int ra0 = A.r[k], ra1 = A.r[k + 1], rb0 = B.r[k], rb1 = B.r[k + 1], nn = A.n[k];
-    const int64_t tot = out.size(k);
-    for (int64_t e = c.tid; e < tot; e += c.nt) {
-      int64_t q = e;
-      const int bb1 = (int)(q % rb1); q /= rb1;
-      const int aa1 = (int)(q % ra1); q /= ra1;
-      const int i = (int)(q % nn); q /= nn;
-      const int bb0 = (int)(q % rb0); q /= rb0;
-      const int aa0 = (int)q;
-      out.c[k][e] = A.c[k][((int64_t)aa0 * nn + i) * ra1 + aa1] * B.c[k][((int64_t)bb0 * nn + i) * rb1 + bb1];
+    // output row (aa0, bb0, i) = outer product of A row (aa0, i, :) and B row
+    // (bb0, i, :); rows to warps, row elements to lanes (32-bit index math)
+    const int rows = ra0 * rb0 * nn, len = ra1 * rb1;
+#if ENGINE_DEVICE
+    const int nw = c.nt >> 5, w = c.tid >> 5, lane = c.tid & 31;
+#else
+    const int nw = 1, w = 0, lane = 0;
+#endif
+    for (int row = w; row < rows; row += nw) {
+      const int i = row % nn, ab = row / nn;
+      const int bb0 = ab % rb0, aa0 = ab / rb0;
+      const double* ar_ = A.c[k] + ((int64_t)aa0 * nn + i) * ra1;
+      const double* br_ = B.c[k] + ((int64_t)bb0 * nn + i) * rb1;
+      double* o = out.c[k] + (int64_t)row * len;
+#if ENGINE_DEVICE
+      for (int col = lane; col < len; col += 32) o[col] = ar_[col / rb1] * br_[col % rb1];
+#else
+      for (int col = 0; col < len; ++col) o[col] = ar_[col / rb1] * br_[col % rb1];
+#endif
     }
   }
   c.sync();
