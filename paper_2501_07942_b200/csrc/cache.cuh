@@ -117,6 +117,8 @@ HDN int cache_init(const Ctx& c, Arena& ar, Cache*& C, int d, const int* n, int6
   return OK;
 }
 
+constexpr int64_t RANK_SORT_MAX = 256;   // cache_eval: rank sort below, bitonic above
+
 // In-place CTA bitonic sort of P (power of two) keys.
 HDN void bitonic_sort(const Ctx& c, Key* a, int64_t P) {
   for (int64_t k = 2; k <= P; k <<= 1) {
@@ -196,7 +198,24 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
     int64_t P = 1;
     while (P < total) P <<= 1;
     Key* sk = mkeys;
-    if (!presorted) {
+    if (!presorted && total <= RANK_SORT_MAX && total * (int64_t)sizeof(Key) <= (int64_t)(SMEM_SCRATCH_DOUBLES * sizeof(double))) {
+      // few misses: stable rank sort (one barrier) instead of the bitonic
+      // network's log^2 P barrier-separated stages; equal keys end adjacent
+      PROF(c, 0);
+      Key* ks = reinterpret_cast<Key*>(sm);
+      for (int64_t i = c.tid; i < total; i += c.nt) ks[i] = mkeys[i];
+      c.sync();
+      for (int64_t i = c.tid; i < total; i += c.nt) {
+        const Key ki = ks[i];
+        int64_t rank = 0;
+        for (int64_t j = 0; j < total; ++j) {
+          const Key kj = ks[j];
+          rank += (key_lt(kj, ki) || (j < i && key_eq(kj, ki))) ? 1 : 0;
+        }
+        mkeys[rank] = ki;
+      }
+      c.sync();
+    } else if (!presorted) {
       PROF(c, 0);
       const bool in_smem = P * (int64_t)sizeof(Key) <= (int64_t)(SMEM_SCRATCH_DOUBLES * sizeof(double));
       if (in_smem) {

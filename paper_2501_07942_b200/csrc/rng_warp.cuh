@@ -15,15 +15,16 @@
 
 namespace tg {
 
+constexpr int JMAX = 160;   // jump table: k = 1..JMAX steps (a CTA looks 128 outputs ahead)
 struct PcgJump {
-  uint64_t a_lo[32], a_hi[32], c_lo[32], c_hi[32];   // k = 1..32 at index k-1
+  uint64_t a_lo[JMAX], a_hi[JMAX], c_lo[JMAX], c_hi[JMAX];   // k = 1..JMAX at index k-1
 };
 
 HD void pcg_make_jump(const Pcg64& g, PcgJump* j) {
   const u128 mult = (((u128)0x2360ED051FC65DA4ULL) << 64) | (u128)0x4385DF649FCCF645ULL;
   const u128 inc = (((u128)g.i_hi) << 64) | g.i_lo;
   u128 A = mult, C = inc;
-  for (int k = 0; k < 32; ++k) {
+  for (int k = 0; k < JMAX; ++k) {
     j->a_lo[k] = (uint64_t)A; j->a_hi[k] = (uint64_t)(A >> 64);
     j->c_lo[k] = (uint64_t)C; j->c_hi[k] = (uint64_t)(C >> 64);
     A = A * mult;
@@ -71,7 +72,7 @@ struct StreamPos {
   uint32_t u32_0;   // that buffered half
 };
 
-HD u128 jump_k(const PcgJump* jt, u128 s, int k) {   // k in [1, 32]
+HD u128 jump_k(const PcgJump* jt, u128 s, int k) {   // k in [1, JMAX]
   const u128 A = (((u128)jt->a_hi[k - 1]) << 64) | jt->a_lo[k - 1];
   const u128 C = (((u128)jt->c_hi[k - 1]) << 64) | jt->c_lo[k - 1];
   return A * s + C;
@@ -83,7 +84,7 @@ HD u128 sp_state(StreamPos& sp, const PcgJump* jt, int64_t steps) {
   return steps == sp.ob ? sp.base : jump_k(jt, sp.base, (int)(steps - sp.ob));
 }
 
-// same, without moving base (per-lane lookahead, steps - ob in [0, 32])
+// same, without moving base (per-thread lookahead, steps - ob in [0, JMAX])
 HD u128 sp_peek(const StreamPos& sp, const PcgJump* jt, int64_t steps) {
   return steps == sp.ob ? sp.base : jump_k(jt, sp.base, (int)(steps - sp.ob));
 }
@@ -104,13 +105,15 @@ HD void sp_seek(StreamPos& sp, const PcgJump* jt, int64_t p) {
 }
 
 // n bounded draws out[t] = bounded(bound(t)), bound(t) in [0, 2^32-2].
-// All CTA threads call; warp 0 works (32 draws per step, lane l evaluating
-// stream value P + l; the first rejection or zero bound ends the accepted
-// run and is resolved uniformly).  g is left as numpy leaves it.
+// All CTA threads work: per round thread l evaluates draw t + l from stream
+// value P + l (jump-ahead from a common base, at most 129 outputs away), the
+// first rejection or zero bound in the round (CTA min) ends the accepted run
+// and is resolved on its own, identically by every thread.  Values written
+// beyond the first rejection are rewritten by later rounds.  g is left as
+// numpy leaves it.
 template <class Bound>
 HDN void warp_draws(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t n, Bound bound, int64_t* out) {
-  const bool w0 = !ENGINE_DEVICE || c.tid < 32;
-  if (w0 && n > 0) {
+  if (n > 0) {
     StreamPos sp;
     sp.g0 = (((u128)g->s_hi) << 64) | g->s_lo;
     sp.base = sp.g0;
@@ -120,57 +123,43 @@ HDN void warp_draws(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t n, Bound 
     int64_t P = 0;   // stream values consumed
     int64_t t = 0;
     while (t < n) {
-      sp_seek(sp, jt, P);
-      const int m = (int)lmin(32, n - t);
-      unsigned rejmask = 0;
-      LANE_LOOP(l) {
-        bool rej = false;
-        if (l < m) {
-          const uint64_t b = bound(t + l);
-          uint64_t res = 0;
-          if (b == 0) rej = true;          // consumes nothing: handled below
-          else rej = !lemire_try(sp_value(sp, jt, P + l), b, &res);
-          if (!rej) out[t + l] = (int64_t)res;
-        }
-#if ENGINE_DEVICE
-        rejmask = __ballot_sync(0xffffffffu, rej);
-#else
-        if (rej) rejmask |= (1u << l);
-#endif
+      // base at the output holding value P: values P .. P + nt - 1 are <= nt/2 + 1 steps away
+      const int64_t o = P < sp.off ? 0 : (P - sp.off) >> 1;
+      while (o - sp.ob > JMAX) { sp.base = jump_k(jt, sp.base, JMAX); sp.ob += JMAX; }
+      if (o > sp.ob) { sp.base = jump_k(jt, sp.base, (int)(o - sp.ob)); sp.ob = o; }
+      const int m = (int)lmin(c.nt, n - t);
+      int first = m;
+      for (int l = c.tid; l < m; l += c.nt) {
+        const uint64_t b = bound(t + l);
+        uint64_t res = 0;
+        const bool rej = b == 0 || !lemire_try(sp_value(sp, jt, P + l), b, &res);
+        if (rej) first = imin(first, l);
+        else out[t + l] = (int64_t)res;
       }
-      int f = m;
-      if (rejmask) {
-#if ENGINE_DEVICE
-        f = __ffs(rejmask) - 1;
-#else
-        f = 0;
-        while (!((rejmask >> f) & 1u)) ++f;
-#endif
-      }
+      const int f = (int)(-block_max(c, -(double)first));
       t += f;
       P += f;
       if (f < m) {
         // draw t: zero bound (no value consumed) or Lemire rejection loop
         const uint64_t b = bound(t);
         if (b == 0) {
-          if (c.leader() || !ENGINE_DEVICE) out[t] = 0;
+          if (c.leader()) out[t] = 0;
         } else {
           while (true) {
-            sp_seek(sp, jt, P);
+            const int64_t o2 = P < sp.off ? 0 : (P - sp.off) >> 1;
+            while (o2 - sp.ob > JMAX) { sp.base = jump_k(jt, sp.base, JMAX); sp.ob += JMAX; }
+            if (o2 > sp.ob) { sp.base = jump_k(jt, sp.base, (int)(o2 - sp.ob)); sp.ob = o2; }
             uint64_t res = 0;
             const bool ok = lemire_try(sp_value(sp, jt, P), b, &res);
             ++P;
             if (ok) {
-              if (c.leader() || !ENGINE_DEVICE) out[t] = (int64_t)res;
+              if (c.leader()) out[t] = (int64_t)res;
               break;
             }
           }
         }
         t += 1;
       }
-#if ENGINE_DEVICE
-      __syncwarp();
-#endif
     }
     // numpy state after the last consumed value
     if (P > 0 && P - 1 >= sp.off) {
@@ -178,14 +167,14 @@ HDN void warp_draws(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t n, Bound 
       const bool low = ((P - 1 - sp.off) & 1) == 0;
       const u128 st = sp_state(sp, jt, o + 1);
       const uint64_t outv = xsl_rr((uint64_t)(st >> 64), (uint64_t)st);
-      if (c.leader() || !ENGINE_DEVICE) {
+      if (c.leader()) {
         g->s_lo = (uint64_t)st;
         g->s_hi = (uint64_t)(st >> 64);
         g->has32 = low ? 1u : 0u;          // low half consumed: high half buffered
         g->u32 = (uint32_t)(outv >> 32);   // buffered half, or the stale consumed one
       }
     } else if (P > 0) {                    // only the buffered half was consumed
-      if (c.leader() || !ENGINE_DEVICE) g->has32 = 0;
+      if (c.leader()) g->has32 = 0;
     }
   }
   c.sync();
@@ -194,7 +183,7 @@ HDN void warp_draws(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t n, Bound 
 struct BoundCols {
   const int* shape;
   int d;
-  HD uint64_t operator()(int64_t t) const { return (uint64_t)(shape[t % d] - 1); }
+  HD uint64_t operator()(int64_t t) const { return (uint64_t)(shape[(int)t % d] - 1); }   // t < 2^31
 };
 struct BoundUp {   // j = lo + t
   int64_t lo;

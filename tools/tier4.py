@@ -22,7 +22,7 @@ sys.path.insert(0, ROOT)
 from paper_2501_07942_b200.configs import BASELINE_CONFIGS, simulate  # noqa: E402
 
 STEPS = {"C1": 3, "C2": 2, "C3": 2}
-RUNS = 256
+RUNS_OF = {"C1": 256, "C2": 256, "C3": 64}   # C3 oracle steps take 2-60 s each
 
 
 def _oracle_run(arg):
@@ -46,13 +46,13 @@ def _oracle_run(arg):
     return run, STEPS[name], mean0
 
 
-def oracle(out):
+def oracle(out, names=None):
     import multiprocessing as mp
-    res = {}
+    res = json.load(open(out)) if os.path.exists(out) else {}
     with mp.get_context("spawn").Pool(max(1, len(os.sched_getaffinity(0)) - 1)) as pool:
-        for name in STEPS:
+        for name in (names or STEPS):
             t0 = time.time()
-            rows = pool.map(_oracle_run, [(name, r) for r in range(RUNS)], chunksize=1)
+            rows = pool.map(_oracle_run, [(name, r) for r in range(RUNS_OF[name])], chunksize=1)
             res[name] = {"fail_step": [int(r[1]) for r in sorted(rows)], "mean0": [r[2] for r in sorted(rows)]}
             print(name, "%.0fs" % (time.time() - t0), flush=True)
             json.dump(res, open(out, "w"))
@@ -62,6 +62,7 @@ def gpu(out):
     from paper_2501_07942_b200.bank import BankConfig, FilterBank
     res = {}
     for name in STEPS:
+        RUNS = RUNS_OF[name]
         cfg = BASELINE_CONFIGS[name]
         g, x = cfg["grid"], cfg["cross"]
         bc = BankConfig(n_per_axis=g["n_per_axis"], sigma_mult=g["sigma_mult"], round_tol=g["round_tol"],
@@ -97,10 +98,13 @@ def compare(a_path, b_path):
     a, b = json.load(open(a_path)), json.load(open(b_path))
     rep = {}
     for name in STEPS:
-        fa, fb = np.array(a[name]["fail_step"]), np.array(b[name]["fail_step"])
+        if name not in a or name not in b:
+            continue
+        RUNS = min(len(a[name]["fail_step"]), len(b[name]["fail_step"]))
+        fa, fb = np.array(a[name]["fail_step"][:RUNS]), np.array(b[name]["fail_step"][:RUNS])
         hist = {int(s): [int((fa == s).sum()), int((fb == s).sum())] for s in range(STEPS[name] + 1)}
         both = [i for i in range(RUNS) if a[name]["mean0"][i] is not None and b[name]["mean0"][i] is not None]
-        rels = [float(np.max(np.abs(np.array(a[name]["mean0"][i]) - a[name]["mean0"][i] * 0 - b[name]["mean0"][i]))
+        rels = [float(np.max(np.abs(np.array(a[name]["mean0"][i]) - np.array(b[name]["mean0"][i])))
                       / np.max(np.abs(a[name]["mean0"][i]))) for i in both]
         rep[name] = {"runs": RUNS, "fail_step_hist_oracle_gpu": hist, "same_fail_step": float(np.mean(fa == fb)),
                      "step0_both_completed": len(both),
@@ -112,7 +116,8 @@ def compare(a_path, b_path):
 
 if __name__ == "__main__":
     if sys.argv[1] == "oracle":
-        oracle(sys.argv[sys.argv.index("--out") + 1])
+        names = sys.argv[sys.argv.index("--configs") + 1].split(",") if "--configs" in sys.argv else None
+        oracle(sys.argv[sys.argv.index("--out") + 1], names)
     elif sys.argv[1] == "gpu":
         gpu(sys.argv[sys.argv.index("--out") + 1])
     else:
