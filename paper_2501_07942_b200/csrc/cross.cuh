@@ -369,6 +369,7 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
       if (nb > 0) { seen = cand[1].err; rbest = cand[1].row; cbest = cand[1].col; }
       sh->i0 = rbest; sh->i1 = cbest; sh->f0 = seen;
     }
+    c.sync();   // publish the leader's pick before anyone reads it
   }
   rbest = sh->i0; cbest = sh->i1; seen = sh->f0;
   nc_ = nb;
