@@ -106,6 +106,7 @@ typedef struct {
   int32_t converged;
 } ttgbf_cross_info;
 
+#define TTGBF_NRANKLOG 10
 #define TTGBF_NMOM (1 + TTGBF_MAXD + TTGBF_MAXD * (TTGBF_MAXD + 1) / 2)
 
 /* per-filter diagnostics (StepDiagnostics, filters.py:164-188) */
@@ -119,8 +120,9 @@ typedef struct {
   int64_t ws_peak;               /* bytes of workspace used */
   /* shape log: ranks of 0 input TT, 1 likelihood cross TT, 2 filtering TT,
    * 3 shifted TT, 4 kernel cross TT, 5 rounded convolution, 6 realign cross
-   * TT, 7 output TT (used for the algorithmic FLOP count) */
-  int32_t ranks[8][TTGBF_MAXD + 1];
+   * TT, 7 output TT (used for the algorithmic FLOP count), 8 likelihood TT
+   * and 9 kernel TT after the exact-rank squeeze (what the products use) */
+  int32_t ranks[TTGBF_NRANKLOG][TTGBF_MAXD + 1];
   /* SM clock cycles of the stage sections (CTA leader): 0 likelihood cross,
    * 1 Hadamard+finalize, 2 moments, 3 interp+finalize, 4 kernel cross,
    * 5 FFT conv+round, 6 realign cross, 7 final finalize */
@@ -132,7 +134,7 @@ typedef struct {
    * 15 negative mass, 16 qr panel, 17 qr trailing update, 18 round R-multiply,
    * 19 round apply_q, 20 fft spectra+product, 21 svd rrqr, 22 rrqr rank sum (count, not cycles), 23 svd_rrqr calls,
    * 24 max rrqr rank (count), 25 svd jacobi, 26 svd U from reflectors, 27 svd Bt QR + V,
-   * 28 svd calls with rank > 64 (count), 29 their cycles, 30-31 spare */
+   * 28 svd calls with rank > 64 (count), 29 their cycles, 30 exact-rank squeeze of cross outputs, 31 spare */
   int64_t prof[32];
   int64_t big_used;       /* steps that borrowed an overflow workspace */
   int64_t big_peak;       /* peak bytes used in an overflow workspace */
@@ -232,7 +234,7 @@ typedef struct {
   double mass_before_norm;
   double clipped_mass;
   int64_t calls[3];
-  int32_t ranks[8][TTGBF_MAXD + 1];
+  int32_t ranks[TTGBF_NRANKLOG][TTGBF_MAXD + 1];
   int64_t cycles;         /* SM clock cycles the step took on its CTA (0 in host emulation) */
 } ttgbf_step_rec;
 

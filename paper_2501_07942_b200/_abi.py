@@ -33,7 +33,7 @@ CROSS_INFO = np.dtype([("achieved", "f8"), ("calls", "i8"), ("sweeps", "i4"), ("
                       align=True)
 DIAG = np.dtype([("status", "i4"), ("outlier", "i4"), ("mass_before_norm", "f8"),
                  ("clipped_mass", "f8"), ("cross", CROSS_INFO, 3), ("raw_moments", "f8", NMOM),
-                 ("ws_peak", "i8"), ("ranks", "i4", (8, MAXD + 1)), ("cycles", "i8", 8),
+                 ("ws_peak", "i8"), ("ranks", "i4", (10, MAXD + 1)), ("cycles", "i8", 8),
                  ("prof", "i8", 32), ("big_used", "i8"), ("big_peak", "i8"),
                  ("big_wait", "i8")], align=True)
 MODEL = np.dtype([("d", "i4"), ("b", "i4"), ("hkind", "i4"), ("nang", "i4"), ("ang", "i4", MAXB),
@@ -46,7 +46,7 @@ GAUSS = np.dtype([("mean", "f8", MAXD), ("LU", "f8", MAXD * MAXD), ("piv", "i4",
 RUN_CFG_FIELDS = None
 STEP_REC = np.dtype([("status", "i4"), ("k", "i4"), ("spd_fixed", "i4"), ("outlier", "i4"), ("mean", "f8", MAXD),
                      ("cov", "f8", MAXD * (MAXD + 1) // 2), ("mass_before_norm", "f8"), ("clipped_mass", "f8"),
-                     ("calls", "i8", 3), ("ranks", "i4", (8, MAXD + 1)), ("cycles", "i8")], align=True)
+                     ("calls", "i8", 3), ("ranks", "i4", (10, MAXD + 1)), ("cycles", "i8")], align=True)
 
 
 def rec_cov(rec, d: int) -> np.ndarray:

@@ -1,9 +1,10 @@
 """Build the sm_100a product library in-tree (paper_2501_07942_b200/_lib/libttgbf.so).
 
-Two translation units, compiled in parallel and linked into one library:
-api.cu (the TT step engine; every csrc/*.cuh) and dense.cu (the dense grid
-filter; common.cuh + measure.cuh only).  Objects are rebuilt only when one
-of their sources is newer.
+Five objects, compiled in parallel and linked into one library: api.cu (the
+TT step engine; every csrc/*.cuh) once per entry-point group
+(-DTTGBF_API_PART=1..4: prior+measurement, time updates, persistent run,
+primitives) and dense.cu (the dense grid filter; common.cuh + measure.cuh
+only).  Objects are rebuilt only when one of their sources is newer.
 """
 
 from __future__ import annotations
@@ -33,15 +34,15 @@ def _srcs(names):
 
 def units():
     cuh = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
-    return {
-        "api": (os.path.join(CSRC, "api.cu"), _srcs(["api.cu"] + cuh)),
-        "dense": (os.path.join(CSRC, "dense.cu"), _srcs(["dense.cu", "common.cuh", "measure.cuh"])),
-    }
+    api = os.path.join(CSRC, "api.cu")
+    out = {f"api{k}": (api, _srcs(["api.cu"] + cuh), [f"-DTTGBF_API_PART={k}"]) for k in (1, 2, 3, 4)}
+    out["dense"] = (os.path.join(CSRC, "dense.cu"), _srcs(["dense.cu", "common.cuh", "measure.cuh"]), [])
+    return out
 
 
 def sources():
     out = set()
-    for _, deps in units().values():
+    for _, deps, _ in units().values():
         out.update(deps)
     return sorted(out)
 
@@ -66,10 +67,11 @@ def build(force: bool = False, verbose: bool = True) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     t0 = time.time()
     procs = {}
-    for name, (src, deps) in units().items():
+    extra = os.environ.get("TTGBF_NVCC_FLAGS", "").split()
+    for name, (src, deps, defs) in units().items():
         obj = _obj(name)
         if force or _stale(obj, deps):
-            cmd = [NVCC] + FLAGS + ["-c", "-o", obj + ".tmp", src]
+            cmd = [NVCC] + FLAGS + defs + extra + ["-c", "-o", obj + ".tmp", src]
             procs[name] = (obj, subprocess.Popen(cmd, cwd=CSRC, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                                  text=True))
     for name, (obj, proc) in procs.items():

@@ -18,6 +18,13 @@
 
 using namespace tg;
 
+// The device build compiles this file once per part (-DTTGBF_API_PART=1..4,
+// in parallel: build.py); part 0 (host emulation) holds every entry point.
+#ifndef TTGBF_API_PART
+#define TTGBF_API_PART 0
+#endif
+#define API_PART(k) (TTGBF_API_PART == 0 || TTGBF_API_PART == (k))
+
 namespace {
 
 #ifdef __CUDACC__
@@ -54,6 +61,7 @@ int launch(int count, F f, void*) {
 
 extern "C" {
 
+#if API_PART(1)
 int ttgbf_version(void) { return 1; }
 int ttgbf_block_threads(void) { return BLOCK_THREADS; }
 int64_t ttgbf_smem_bytes(void) { return (int64_t)SMEM_DOUBLES * 8; }
@@ -115,7 +123,9 @@ int ttgbf_filter_measure(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cr
   };
   return launch(nfilt, f, stream);
 }
+#endif
 
+#if API_PART(2)
 int ttgbf_filter_time_update(const ttgbf_model* model, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
                              const ttgbf_filter_io* io, int nfilt, const int32_t* probes, int nprobes,
                              const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr, double* state,
@@ -155,7 +165,9 @@ int ttgbf_filter_time_update_std(const ttgbf_model* model, ttgbf_grid_cfg gcfg, 
   };
   return launch(nfilt, f, stream);
 }
+#endif
 
+#if API_PART(3)
 int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_grid_cfg gcfg, ttgbf_cross_cfg xcfg,
                      ttgbf_run_cfg rcfg, ttgbf_filter_io* io, int32_t* kstep, const double* Z, int nfilt,
                      const int32_t* probes, int nprobes, const int32_t* seeds, int nseeds, ttgbf_tt* state_hdr,
@@ -227,7 +239,9 @@ int ttgbf_filter_run(const ttgbf_model* model, const ttgbf_gauss* prior, ttgbf_g
   };
   return launch(nslots < nfilt ? nslots : nfilt, f, stream);
 }
+#endif
 
+#if API_PART(4)
 // ---------------------------------------------------------------- TT primitives
 int ttgbf_tt_round(const ttgbf_tt* in_hdr, const double* in, int64_t in_cap, int count, double tol, int max_rank,
                    ttgbf_tt* out_hdr, double* out, int64_t out_cap, void* ws, int64_t ws_bytes, int32_t* status,
@@ -361,7 +375,9 @@ int ttgbf_eval_blackbox(int kind, const ttgbf_model* model, const ttgbf_gauss* p
   };
   return launch(count, f, stream);
 }
+#endif
 
+#if API_PART(1)
 int64_t ttgbf_sizeof(int which) {
   switch (which) {
     case 0: return (int64_t)sizeof(ttgbf_axis);
@@ -377,6 +393,7 @@ int64_t ttgbf_sizeof(int which) {
     default: return -1;
   }
 }
+#endif
 
 }  // extern "C"
 

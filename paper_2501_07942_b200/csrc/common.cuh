@@ -17,7 +17,7 @@
 #ifdef __CUDACC__
 #define HD __host__ __device__ __forceinline__
 #define HDI __host__ __device__
-#define HDN __host__ __device__ __noinline__
+#define HDN static __host__ __device__ __noinline__   // internal linkage: api.cu is compiled once per entry-point group
 #else
 #define HD inline
 #define HDI

@@ -107,6 +107,33 @@ HDN int tt_compact(const Ctx& c, Arena& ar, size_t mark, TT& t) {
   return OK;
 }
 
+// Exact-rank squeeze of a cross output.  greedy_cross returns cores solved
+// from rank-deficient skeleton systems, so about half of its bond directions
+// are numerically null (singular values at 1e-16 of the largest; measured on
+// the C3 kernel and likelihood crosses).  Dropping them before the Kronecker
+// product (FFT convolution, Hadamard) changes the tensor by <= SQUEEZE_TOL
+// relative -- rounding noise next to the 1e-8 rounding that follows -- and
+// shrinks the product cores ~4x.  `t` must be the last allocation, at `mark`.
+#ifndef TTGBF_SQUEEZE
+#define TTGBF_SQUEEZE 1
+#endif
+constexpr double SQUEEZE_TOL = 1e-14;
+HDN int tt_squeeze(const Ctx& c, Arena& ar, size_t mark, TT& t, double* sm) {
+#if TTGBF_SQUEEZE
+  int maxr = 1;
+  for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
+  if (maxr == 1) return OK;
+  PROF(c, 30);
+  TT r;
+  CK(tt_round(c, ar, t, SQUEEZE_TOL, 0, r, sm, true));
+  CK(tt_compact(c, ar, mark, r));
+  t = r;
+#else
+  (void)c; (void)ar; (void)mark; (void)t; (void)sm;
+#endif
+  return OK;
+}
+
 HD CrossCfg make_cross_cfg(const ttgbf_cross_cfg& x, const int32_t* seeds, int nseeds) {
   CrossCfg cc;
   cc.tol = x.tol;
@@ -324,6 +351,8 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
     CK(greedy_cross(c, ar, *sp, make_cross_cfg(xcfg, seeds, nseeds), S.xs, lik, &ci, S.sm));
     if (c.leader()) { put_cross(&dg->cross[0], ci); log_ranks(dg, 1, lik); }
     CK(tt_compact(c, ar, mk, lik));
+    CK(tt_squeeze(c, ar, mk, lik, S.sm));
+    if (c.leader()) log_ranks(dg, 8, lik);
     const int64_t t1 = clk();
     if (c.leader()) dg->cycles[0] += t1 - t0;
     t0 = t1;
@@ -442,6 +471,9 @@ HDN int stage_time(const Ctx& c, Arena& ar, const ttgbf_model& model, const ttgb
   if (c.leader()) { put_cross(&dg->cross[1], ci); log_ranks(dg, 4, ker); dg->cycles[4] += clk() - t0; }
   t0 = clk();
   CK(tt_compact(c, ar, m1, ker));
+  CK(tt_squeeze(c, ar, m1, ker, S.sm));
+  if (c.leader()) { log_ranks(dg, 9, ker); dg->cycles[4] += clk() - t0; }
+  t0 = clk();
   // FFT convolution + rounding
   TT conv;
   int64_t pbytes = 0;
@@ -595,7 +627,7 @@ HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
     dg->outlier = 0;
     R->k = kk;
     for (int q = 0; q < 3; ++q) dg->cross[q].calls = 0;
-    for (int sl = 0; sl < 8; ++sl)
+    for (int sl = 0; sl < TTGBF_NRANKLOG; ++sl)
       for (int k = 0; k <= TTGBF_MAXD; ++k) dg->ranks[sl][k] = 0;
   }
   c.sync();
@@ -632,7 +664,7 @@ HDN int stage_run_step(const Ctx& c, Arena& ar, const ttgbf_model& model, const 
     R->mass_before_norm = dg->mass_before_norm;
     R->clipped_mass = dg->clipped_mass;
     for (int q = 0; q < 3; ++q) R->calls[q] = dg->cross[q].calls;
-    for (int sl = 0; sl < 8; ++sl)
+    for (int sl = 0; sl < TTGBF_NRANKLOG; ++sl)
       for (int k = 0; k <= TTGBF_MAXD; ++k) R->ranks[sl][k] = dg->ranks[sl][k];
     R->cycles = clk() - t_start;
     if (st) {

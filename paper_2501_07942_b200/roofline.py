@@ -52,14 +52,31 @@ def cross_flops(calls, ranks, n, per_eval):
     return f
 
 
-def step_flops(dm_row, dt_row, d, b, n):
-    """(measure_flops, time_update_flops) for one filter step."""
+def _squeezed(row, slot, d, full):
+    """Ranks after the engine's exact-rank squeeze (log slots 8 / 9) when logged."""
+    ranks = row["ranks"]
+    if len(ranks) <= slot or not int(ranks[slot][0]):
+        return full
+    return [int(v) for v in ranks[slot][: d + 1]]
+
+
+def step_flops(dm_row, dt_row, d, b, n, executed=False):
+    """(measure_flops, time_update_flops) for one filter step.
+
+    executed=False: the reference algorithm's work (products of
+    the cross outputs as they come).  executed=True: the same formulas on the
+    ranks the engine's products actually have after the exact-rank squeeze of
+    the likelihood / kernel TTs (plus the squeeze's own rounding)."""
     rin = _r(dm_row, 0, d)
     rlik = _r(dm_row, 1, d)
     rfil = _r(dm_row, 2, d)
     fm = 0.0
     if rlik[0]:
         fm += cross_flops(int(dm_row["cross"][0]["calls"]), rlik, n, 2 * b * b + 10 * b + d)
+        if executed:
+            rsq = _squeezed(dm_row, 8, d, rlik)
+            fm += round_flops(rlik, n, rsq)
+            rlik = rsq
         prod = [a * c for a, c in zip(rin, rlik)]
         fm += chain_size(prod, n)                                  # Hadamard
         fm += round_flops(prod, n, rfil)
@@ -72,6 +89,10 @@ def step_flops(dm_row, dt_row, d, b, n):
     rout = _r(dt_row, 7, d)
     ft = 4.0 * chain_size(rfil, n) + round_flops(rfil, n, rsh)    # interp + finalize
     ft += cross_flops(int(dt_row["cross"][1]["calls"]), rker, n, 2 * d * d + 2 * d + 10)
+    if executed:
+        rsq = _squeezed(dt_row, 9, d, rker)
+        ft += round_flops(rker, n, rsq)
+        rker = rsq
     prod = [a * c for a, c in zip(rker, rsh)]
     fib = sum(rker[k] * rker[k + 1] + rsh[k] * rsh[k + 1] for k in range(d))
     ft += 5.0 * n * math.log2(n) * fib + 6.0 * chain_size(prod, n) + 5.0 * n * math.log2(n) * sum(
@@ -143,7 +164,7 @@ class _Row:
         return self.rec[key]
 
 
-def rec_flops(rec, d, b, n):
+def rec_flops(rec, d, b, n, executed=False):
     """(measure, time) algorithmic FLOPs of one persistent-run step record."""
     r = _Row(rec)
-    return step_flops(r, r, d, b, n)
+    return step_flops(r, r, d, b, n, executed)
