@@ -93,7 +93,8 @@ class Clocks:
         cmd = ["nvidia-smi", "-i", str(self.index),
                "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+               "utilization.gpu,utilization.memory",
                "--format=csv,noheader,nounits", "-lms", "200"]
         try:
             self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
@@ -123,8 +124,12 @@ class Clocks:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 4 + i and s[4 + i].lower() == "active"})
+        pw = [float(s[2]) for s in self.samples if len(s) > 2 and s[2].replace(".", "").isdigit()]
+        mem = [float(s[9]) for s in self.samples if len(s) > 9 and s[9].isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_median": float(np.median(pw)) if pw else None,
+                "mem_util_pct_median": float(np.median(mem)) if mem else None}
 
 
 # ---------------------------------------------------------------------------

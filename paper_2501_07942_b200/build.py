@@ -18,7 +18,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIBDIR = os.path.join(HERE, "_lib")
-OUT = os.path.join(LIBDIR, "libttgbf.so")
+# tuning variants: TTGBF_LIB_VARIANT=tag TTGBF_NVCC_FLAGS="-D..." -> libttgbf_tag.so (loaded by _abi with the same tag)
+VARIANT = os.environ.get("TTGBF_LIB_VARIANT", "")
+OUT = os.path.join(LIBDIR, "libttgbf%s.so" % ("_" + VARIANT if VARIANT else ""))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 HEADER = os.path.join(ROOT, "include", "ttgbf.h")
 
@@ -48,7 +50,7 @@ def sources():
 
 
 def _obj(name):
-    return os.path.join(LIBDIR, f"{name}.o")
+    return os.path.join(LIBDIR, f"{name}{'_' + VARIANT if VARIANT else ''}.o")
 
 
 def _stale(path, deps):
@@ -79,7 +81,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
         if proc.returncode != 0:
             sys.stderr.write(log)
             raise RuntimeError(f"nvcc failed compiling {name}.cu")
-        with open(os.path.join(LIBDIR, f"ptxas_{name}.log"), "w") as f:
+        with open(os.path.join(LIBDIR, f"ptxas_{name}{'_' + VARIANT if VARIANT else ''}.log"), "w") as f:
             f.write(log)
         os.replace(obj + ".tmp", obj)
     tmp = OUT + ".tmp"

@@ -198,13 +198,31 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
     int64_t P = 1;
     while (P < total) P <<= 1;
     Key* sk = mkeys;
-    if (!presorted && total <= RANK_SORT_MAX && total * (int64_t)sizeof(Key) <= (int64_t)(SMEM_SCRATCH_DOUBLES * sizeof(double))) {
+    if (!presorted && total <= RANK_SORT_MAX && (!ENGINE_DEVICE || total <= c.nt) && total * (int64_t)sizeof(Key) <= (int64_t)(SMEM_SCRATCH_DOUBLES * sizeof(double))) {
       // few misses: stable rank sort (one barrier) instead of the bitonic
       // network's log^2 P barrier-separated stages; equal keys end adjacent
       PROF(c, 0);
       Key* ks = reinterpret_cast<Key*>(sm);
       for (int64_t i = c.tid; i < total; i += c.nt) ks[i] = mkeys[i];
       c.sync();
+#if ENGINE_DEVICE
+      // L = 2^k lanes share one key's comparisons (L * total <= blockDim)
+      int L = 1;
+      while (L < 32 && 2 * L * total <= c.nt) L <<= 1;
+      {
+        const int i = c.tid / L, sub = c.tid % L;
+        const bool act = i < total;
+        const Key ki = ks[act ? i : 0];
+        int rank = 0;
+        if (act)
+          for (int j = sub; j < (int)total; j += L) {
+            const Key kj = ks[j];
+            rank += (key_lt(kj, ki) || (j < i && key_eq(kj, ki))) ? 1 : 0;
+          }
+        for (int o = L >> 1; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+        if (act && sub == 0) mkeys[rank] = ki;
+      }
+#else
       for (int64_t i = c.tid; i < total; i += c.nt) {
         const Key ki = ks[i];
         int64_t rank = 0;
@@ -214,6 +232,7 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
         }
         mkeys[rank] = ki;
       }
+#endif
       c.sync();
     } else if (!presorted) {
       PROF(c, 0);

@@ -201,10 +201,9 @@ HDN int x_solve_core(const Ctx& c, Arena& ar, XState& s, int k, double* sm) {
   ALLOC(cn, double, r + 1, ar);
   ALLOC(jpvt, int, r, ar);
   // A_ls = ahat^T: (i,j) -> ahat[j][i]; B(i, row) = fib[row*cc + i]
-  (void)sm;
   int rank_used = 0;
   CK(lstsq_pivoted(c, s.ahat[k + 1], 1, s.maxr, r, s.fib[k], cc, A * n, s.core[k], cc, W, W2, tau, tau2, jpvt,
-                   cn, &rank_used));
+                   cn, &rank_used, sm, SMEM_SCRATCH_DOUBLES));
 #if defined(ENGINE_HOSTSIM) && defined(ENGINE_TRACE)
   {
     double cs = 0.0;
@@ -337,10 +336,7 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
     warp_choice(c, &sh->rng, rws.jt, g.nrow, qr, cr, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
     warp_choice(c, &sh->rng, rws.jt, g.ncol, qc, cc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
   }
-  if (c.leader()) {
-    for (int i = 0; i < qr; ++i)
-      for (int j = 0; j < qc; ++j) { br[i * qc + j] = cr[i]; bc[i * qc + j] = cc[j]; }
-  }
+  for (int e = c.tid; e < qr * qc; e += c.nt) { br[e] = cr[e / qc]; bc[e] = cc[e % qc]; }
   c.sync();
   const int nb = qr * qc;
   CK(x_errors(c, ar, C, spec, s, g, br, bc, nb, e, sm));
@@ -381,14 +377,11 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
       PROF(c, 10);
       warp_choice(c, &sh->rng, rws.jt, g.nrow, X_SCAN, br, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
     }
-    if (c.leader()) {
-      if (g.nrow > X_SCAN) nsr = X_SCAN;
-      else { for (int i = 0; i < g.nrow; ++i) br[i] = i; nsr = g.nrow; }
-      for (int i = 0; i < nsr; ++i) bc[i] = cbest;
-      sh->i2 = nsr;
-    }
+    nsr = imin(g.nrow, X_SCAN);
+    if (g.nrow <= X_SCAN)
+      for (int i = c.tid; i < nsr; i += c.nt) br[i] = i;
+    for (int i = c.tid; i < nsr; i += c.nt) bc[i] = cbest;
     c.sync();
-    nsr = (int)sh->i2;
     CK(x_errors(c, ar, C, spec, s, g, br, bc, nsr, e, sm));
     ValIdx best{-1.0, 0};
     for (int i = c.tid; i < nsr; i += c.nt) best = vi_better(best, ValIdx{e[i], i});
@@ -401,14 +394,11 @@ HDN int x_hunt(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, XState& 
       PROF(c, 10);
       warp_choice(c, &sh->rng, rws.jt, g.ncol, X_SCAN, bc, rws.disp, rws.touch, rws.draws, rws.flags, reinterpret_cast<uint32_t*>(sm), 2 * SMEM_SCRATCH_DOUBLES, rws.gset);
     }
-    if (c.leader()) {
-      if (g.ncol > X_SCAN) nsc = X_SCAN;
-      else { for (int i = 0; i < g.ncol; ++i) bc[i] = i; nsc = g.ncol; }
-      for (int i = 0; i < nsc; ++i) br[i] = rnew;
-      sh->i2 = nsc;
-    }
+    nsc = imin(g.ncol, X_SCAN);
+    if (g.ncol <= X_SCAN)
+      for (int i = c.tid; i < nsc; i += c.nt) bc[i] = i;
+    for (int i = c.tid; i < nsc; i += c.nt) br[i] = rnew;
     c.sync();
-    nsc = (int)sh->i2;
     CK(x_errors(c, ar, C, spec, s, g, br, bc, nsc, e, sm));
     ValIdx best2{-1.0, 0};
     for (int i = c.tid; i < nsc; i += c.nt) best2 = vi_better(best2, ValIdx{e[i], i});

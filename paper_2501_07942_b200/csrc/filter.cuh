@@ -167,7 +167,9 @@ HDN int finalize_tt(const Ctx& c, Arena& ar, TT& t, const ttgbf_grid_cfg& g, con
   const double dv = cell_volume(steps, d);
   const size_t mk = ar.mark();
   double* ws;
-  ALLOC(ws, double, 4 * 1024 + 16, ar);
+  int wr = 1;
+  for (int k = 0; k <= d; ++k) wr = imax(wr, t.r[k]);
+  ALLOC(ws, double, 2 * wr + 1024, ar);   // tt_sum: 2 * maxr + blockDim
   TT r;
   if (g.normalize_before_round) {
     const double mass = tt_sum(c, t, ws) * dv;
@@ -364,7 +366,9 @@ HDN int stage_measure(const Ctx& c, Arena& ar, const ttgbf_model& model, const t
       TT prod;
       CK(tt_hadamard(c, A, p, lik, prod));
       double* ws;
-      ALLOC(ws, double, 4096 + 16, A);
+      int wr = 1;
+      for (int k = 0; k <= d; ++k) wr = imax(wr, prod.r[k]);
+      ALLOC(ws, double, 2 * wr + 1024, A);   // tt_sum: 2 * maxr + blockDim
       const double mass = tt_sum(c, prod, ws) * cell_volume(steps, d);
       if (!isfinite(mass) || mass <= MASS_FLOOR) {
         if (c.leader()) dg->outlier = 1;

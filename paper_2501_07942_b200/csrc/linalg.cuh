@@ -739,7 +739,21 @@ HD void laic1(int job, int j, const double* x, double sest, const double* w, dou
 // ---------------------------------------------------------------------------
 HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_c, int r, const double* B,
                       int64_t ldb, int nrhs, double* X, int64_t ldx, double* W, double* W2, double* tau, double* tau2,
-                      int* jpvt, double* cn, int* rank_out) {
+                      int* jpvt, double* cn, int* rank_out, double* sm = nullptr, int sm_doubles = 0) {
+  // Small systems (2 r^2 + 4 r + 2 doubles fit the CTA scratch) are factored
+  // in shared memory: the pivot search, swaps, reflectors and condition
+  // estimation below are chains of dependent loads, and every thread of the
+  // solve phase reads all of R.  Same arithmetic in the same order as the
+  // global-memory path.
+  if (sm && 2 * (int64_t)r * r + 4 * r + 2 <= sm_doubles) {
+    W = sm;
+    W2 = sm + (int64_t)r * r;
+    cn = W2 + (int64_t)r * r;
+    tau = cn + r + 1;
+    tau2 = tau + r;
+    jpvt = reinterpret_cast<int*>(tau2 + r);
+    c.sync();
+  }
   for (int64_t e = c.tid; e < (int64_t)r * r; e += c.nt) {
     int i = (int)(e % r), j = (int)(e / r);
     W[i + (int64_t)j * r] = A[i * lda_r + j * lda_c];
@@ -777,20 +791,42 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
     WSYNC();
     const double tol3z = sqrt(LA_EPS);
     for (int j = 0; j < r; ++j) {
-      if (lane == 0) {
-        int best = j;
-        for (int q = j + 1; q < r; ++q)
-          if (fabs(cn[q]) > fabs(cn[best])) best = q;   // idamax: first max
-        if (best != j) {
-          for (int i = 0; i < r; ++i) {
-            const double t = W[i + (int64_t)j * r];
-            W[i + (int64_t)j * r] = W[i + (int64_t)best * r];
-            W[i + (int64_t)best * r] = t;
-          }
+      // idamax (first max) over cn[j..r): lanes scan strided, ties to the lower index
+      int best = j;
+#if ENGINE_DEVICE
+      {
+        double bv = -1.0;
+        int bi = r;
+        for (int q = j + lane; q < r; q += L) {
+          const double v = fabs(cn[q]);
+          if (v > bv) { bv = v; bi = q; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+        }
+        // (a NaN norm never compares greater: the serial scan keeps j as well)
+        best = (bi < r && bv > fabs(cn[j])) ? bi : j;
+      }
+#else
+      for (int q = j + 1; q < r; ++q)
+        if (fabs(cn[q]) > fabs(cn[best])) best = q;
+#endif
+      if (best != j) {
+        for (int i = lane; i < r; i += L) {
+          const double t = W[i + (int64_t)j * r];
+          W[i + (int64_t)j * r] = W[i + (int64_t)best * r];
+          W[i + (int64_t)best * r] = t;
+        }
+        if (lane == 0) {
           const int t = jpvt[j]; jpvt[j] = jpvt[best]; jpvt[best] = t;
           cn[best] = cn[j];
           tau2[best] = tau2[j];
         }
+      }
+      WSYNC();
+      if (lane == 0) {
         double t2 = 0.0;
         if (j < r - 1) larfg_lapack(r - j - 1, &W[j + (int64_t)j * r], W + j + 1 + (int64_t)j * r, 1, &t2);
         tau[j] = t2;
@@ -897,7 +933,10 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
   const double xscl = cn[r] / bscl;   // X = (A-scale / B-scale) * solution of the scaled system
   // per right-hand side: y = Q^T b; triangular / min-norm solve; permute
   for (int q = c.tid; q < nrhs; q += c.nt) {
-    double yy[X_MAXR_SOLVE], sol[X_MAXR_SOLVE];
+    // one private vector per thread, solved in place (y -> solution): half
+    // the local-memory footprint of separate y / solution arrays
+    double yy[X_MAXR_SOLVE];
+    double* sol = yy;
     for (int i = 0; i < r; ++i) yy[i] = B[i + (int64_t)q * ldb] * bscl;
     for (int j = 0; j < r; ++j) {
       const double t2 = tau[j];
@@ -919,14 +958,13 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
       }
     } else {
       // [R11 R12] = L2^T Q2^T with W2 = Q2 L2 (L2 upper, rank x rank)
-      // solve L2^T w = y[0:rank] (forward), sol = Q2 [w; 0]
-      double wv[X_MAXR_SOLVE];
+      // solve L2^T w = y[0:rank] (forward, in place), sol = Q2 [w; 0]
       for (int i = 0; i < rank; ++i) {
         double s2 = yy[i];
-        for (int k = 0; k < i; ++k) s2 -= W2[k + (int64_t)i * r] * wv[k];
-        wv[i] = s2 / W2[i + (int64_t)i * r];
+        for (int k = 0; k < i; ++k) s2 -= W2[k + (int64_t)i * r] * yy[k];
+        yy[i] = s2 / W2[i + (int64_t)i * r];
       }
-      for (int i = 0; i < r; ++i) sol[i] = (i < rank) ? wv[i] : 0.0;
+      for (int i = rank; i < r; ++i) sol[i] = 0.0;
       for (int j = rank - 1; j >= 0; --j) {
         const double t2 = tau2[j];
         if (t2 == 0.0) continue;

@@ -269,6 +269,8 @@ HD void swap_resolve(const Ctx& c, int64_t ns, IFn I, JFn J, Get get, Set set, F
   }
 }
 
+HDN int64_t scan_offsets(const Ctx& c, int64_t mine, int64_t* total);   // cache.cuh
+
 // rng.choice(pop, size, replace=False) with pre-drawn bounds.
 // disp: >= pop int32 all -1 (restored); touch, draws: >= size int64;
 // flags: >= size bytes; sset: shared scratch (sset_words32 uint32);
@@ -282,16 +284,51 @@ HDN void warp_choice(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t pop, int
     const int64_t ns = pop - first;
     warp_draws(c, g, jt, ns, BoundDown{pop - 1}, draws);   // draw t: j for i = pop-1-t
     const int64_t lo = pop - size;
+    // Step t puts the value found at j_t into position i_t = pop-1-t and the
+    // value of i_t into j_t.  A step whose j_t is drawn once and lies below
+    // the i-range [first, pop) never meets another step: nobody else writes
+    // j_t before it reads it (so it reads j_t itself), and what it writes
+    // there is never read.  Those steps (the bulk: pop >> ns) are resolved by
+    // all threads at once; only the steps with a repeated j or a j inside
+    // the i-range are replayed in order (they read positions that only steps
+    // of the same kind write).
+    for (int64_t t = c.tid; t < ns; t += c.nt) flags[t] = draws[t] >= first ? 1 : 0;
+    c.sync();
+    for (int64_t t = c.tid; t < ns; t += c.nt) {
+      const int64_t j = draws[t];
+#if ENGINE_DEVICE
+      const int32_t prev = atomicCAS(&disp[j], -1, -2 - (int32_t)t);
+#else
+      const int32_t prev = disp[j];
+      if (prev == -1) disp[j] = -2 - (int32_t)t;
+#endif
+      if (prev != -1) { flags[t] = 1; flags[-2 - prev] = 1; }   // both the claimer and the repeat
+    }
+    c.sync();
+    for (int64_t t = c.tid; t < ns; t += c.nt) disp[draws[t]] = -1;
+    c.sync();
+    // in-order list of the interacting steps (touch[0..nc))
+    const int64_t chunk = (ns + c.nt - 1) / c.nt;
+    const int64_t t0 = lmin(ns, chunk * c.tid), t1 = lmin(ns, t0 + chunk);
+    int64_t mine = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+      if (flags[t]) ++mine;
+      else if (pop - 1 - t >= lo) out[pop - 1 - t - lo] = draws[t];
+    }
+    int64_t nc = 0;
+    int64_t off = scan_offsets(c, mine, &nc);
+    for (int64_t t = t0; t < t1; ++t)
+      if (flags[t]) touch[off++] = t;
+    c.sync();
     swap_resolve(
-        c, ns, [=](int64_t t) { return pop - 1 - t; }, [=](int64_t t) { return draws[t]; },
+        c, nc, [=](int64_t q) { return pop - 1 - touch[q]; }, [=](int64_t q) { return draws[touch[q]]; },
         [=](int64_t pos) { const int32_t v = disp[pos]; return v < 0 ? pos : (int64_t)v; },
         [=](int64_t pos, int64_t v) { disp[pos] = (int32_t)v; },
-        [=](int64_t t, int64_t pos, int64_t v) {
+        [=](int64_t, int64_t pos, int64_t v) {
           if (pos >= lo) out[pos - lo] = v;
-          touch[t] = draws[t];
         });
     c.sync();
-    for (int64_t q = c.tid; q < ns; q += c.nt) disp[touch[q]] = -1;
+    for (int64_t q = c.tid; q < nc; q += c.nt) disp[draws[touch[q]]] = -1;
     c.sync();
     return;
   }

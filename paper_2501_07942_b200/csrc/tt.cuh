@@ -45,24 +45,48 @@ HDN int tt_clone(const Ctx& c, Arena& ar, const TT& src, TT& dst) {
 // sum of all entries (tensor_train.py:283-288): v = 1; v = v @ core.sum(1)
 // ---------------------------------------------------------------------------
 HDN double tt_sum(const Ctx& c, const TT& t, double* ws) {
-  // ws: 2 * maxr doubles
+  // ws: 2 * maxr + blockDim doubles
   int maxr = 1;
   for (int k = 0; k <= t.d; ++k) maxr = imax(maxr, t.r[k]);
   double* v = ws;
   double* w = ws + maxr;
+  double* part = ws + 2 * maxr;   // partial sums of the narrow-bond path
   if (c.leader()) v[0] = 1.0;
   c.sync();
   for (int k = 0; k < t.d; ++k) {
     const int rl = t.r[k], n = t.n[k], rr = t.r[k + 1];
-    for (int b = c.tid; b < rr; b += c.nt) {
-      double acc = 0.0;
-      for (int a = 0; a < rl; ++a) {
-        const double* p = t.c[k] + (int64_t)a * n * rr + b;
-        double s = 0.0;
-        for (int i = 0; i < n; ++i) s += p[(int64_t)i * rr];
-        acc = fma(v[a], s, acc);
+    if (2 * rr <= c.nt) {
+      // narrow right bond: G = nt / rr thread groups share the left index
+      // (group g takes a = g, g + G, ...), partials summed in group order
+      const int G = c.nt / rr;
+      const int g = c.tid / rr, b = c.tid % rr;
+      if (g < G) {
+        double acc = 0.0;
+        for (int a = g; a < rl; a += G) {
+          const double* p = t.c[k] + (int64_t)a * n * rr + b;
+          double s = 0.0;
+          for (int i = 0; i < n; ++i) s += p[(int64_t)i * rr];
+          acc = fma(v[a], s, acc);
+        }
+        part[g * rr + b] = acc;
       }
-      w[b] = acc;
+      c.sync();
+      if (c.tid < rr) {
+        double acc = 0.0;
+        for (int q = 0; q < G; ++q) acc += part[q * rr + c.tid];
+        w[c.tid] = acc;
+      }
+    } else {
+      for (int b = c.tid; b < rr; b += c.nt) {
+        double acc = 0.0;
+        for (int a = 0; a < rl; ++a) {
+          const double* p = t.c[k] + (int64_t)a * n * rr + b;
+          double s = 0.0;
+          for (int i = 0; i < n; ++i) s += p[(int64_t)i * rr];
+          acc = fma(v[a], s, acc);
+        }
+        w[b] = acc;
+      }
     }
     c.sync();
     double* tmp = v; v = w; w = tmp;
