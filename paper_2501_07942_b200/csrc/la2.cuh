@@ -415,14 +415,21 @@ __device__ __noinline__ void gemm_cmvw_dev(const Ctx& c, int64_t mr, int jb, int
 // CTA reduction of a small vector (nv <= 33): every thread passes its
 // partials in v[]; the totals are written to out[] (shared) and returned
 // after a barrier.  Deterministic order.
-HD void block_reduce_vec(const Ctx& c, double* v, int nv, double* out) {
+// The array is taken by reference and walked by a fully unrolled loop so it
+// stays in registers (a runtime-bounded loop over v[] would force the
+// caller's accumulators into local memory).
+template <int NV>
+HD void block_reduce_vec(const Ctx& c, double (&v)[NV], int nv, double* out) {
 #if ENGINE_DEVICE
   const int w = c.tid >> 5, l = c.tid & 31, nw = c.nt >> 5;
   double* part = c.red + 64;   // nw x 33 (scan buffer region)
-  for (int q = 0; q < nv; ++q) {
-    double x = v[q];
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (l == 0) part[w * 33 + q] = x;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    if (q < nv) {
+      double x = v[q];
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (l == 0) part[w * 33 + q] = x;
+    }
   }
   __syncthreads();
   if (c.tid < nv) {
@@ -515,6 +522,7 @@ HDN void qr_panel_nb(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
 #ifndef TTGBF_QR_UNROLL
 #define TTGBF_QR_UNROLL 4
 #endif
+template <int PW>
 HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb, double* tau, double* T,
                      double* sm) {
   constexpr int QU = TTGBF_QR_UNROLL;   // rows per thread per iteration
@@ -525,9 +533,9 @@ HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
     double* col = A + (int64_t)j * lda;
     if (jj > 0) {
       // pass A: w_q = V_q^T a_j, V_q = e_{j0+q} + A_q[r > j0+q]
-      double w[NB];
+      double w[PW];
 #pragma unroll
-      for (int q = 0; q < NB; ++q) w[q] = 0.0;
+      for (int q = 0; q < PW; ++q) w[q] = 0.0;
       // QU rows per iteration: their loads are independent, so each thread
       // keeps QU x (jj + 1) loads in flight (the panel streams from L2/HBM)
       for (int64_t r0 = j0 + 1 + c.tid; r0 < m; r0 += (int64_t)QU * c.nt) {
@@ -538,7 +546,7 @@ HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
           x[u] = r < m ? col[r] : 0.0;
         }
 #pragma unroll
-        for (int q = 0; q < NB; ++q)
+        for (int q = 0; q < PW; ++q)
           if (q < jj) {
             const double* aq = A + (int64_t)(j0 + q) * lda;
 #pragma unroll
@@ -558,9 +566,9 @@ HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
       c.sync();
     }
     // pass B: a_j -= V u (rows >= j0); norm^2 and V^T a_j below row j
-    double v[NB + 1];
+    double v[PW + 1];
 #pragma unroll
-    for (int q = 0; q <= NB; ++q) v[q] = 0.0;
+    for (int q = 0; q <= PW; ++q) v[q] = 0.0;
     for (int64_t r0 = j0 + c.tid; r0 < m; r0 += (int64_t)QU * c.nt) {
       double x[QU];
 #pragma unroll
@@ -570,7 +578,7 @@ HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
       }
       if (jj > 0) {
 #pragma unroll
-        for (int q = 0; q < NB; ++q)
+        for (int q = 0; q < PW; ++q)
           if (q < jj) {
             const int64_t dq = j0 + q;
             const double* aq = A + dq * lda;
@@ -595,7 +603,7 @@ HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
         if (r < m && r > j) {
           v[0] = fma(x[u2], x[u2], v[0]);
 #pragma unroll
-          for (int q = 0; q < NB; ++q)
+          for (int q = 0; q < PW; ++q)
             if (q < jj) v[1 + q] = fma(A[(int64_t)(j0 + q) * lda + r], x[u2], v[1 + q]);
         }
       }
@@ -718,7 +726,10 @@ constexpr int NS = TTGBF_QR_NS;   // sub-panel width of the two-level panel fact
 #endif
 HDN void qr_panel_blk(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb, double* tau, double* T, double* sm) {
 #if TTGBF_QR_PANEL_LL
-  qr_panel_ll(c, A, lda, m, j0, jb, tau, T, sm);
+  // register arrays sized to the panel: sub-panels (jb <= 8) keep their 8 + 9
+  // accumulators in registers; the 32-wide instance spills part of them
+  if (jb <= 8) qr_panel_ll<8>(c, A, lda, m, j0, jb, tau, T, sm);
+  else qr_panel_ll<NB>(c, A, lda, m, j0, jb, tau, T, sm);
 #else
   qr_panel_nb(c, A, lda, m, j0, jb, tau, T, sm);
 #endif
