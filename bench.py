@@ -264,13 +264,16 @@ def run_reference(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 def dram_traffic_per_step():
-    """DRAM bytes per attempted filter step of ttgbf_filter_run, from the committed
-    ncu capture (dram__bytes_read.sum + dram__bytes_write.sum, profiles/)."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_dram_c5.json")
-    if not os.path.exists(path):
+    """DRAM bytes per attempted filter step of ttgbf_filter_run, from the newest
+    committed ncu capture (dram__bytes_read.sum + dram__bytes_write.sum of a
+    296-filter one-step launch, profiles/rNN_ncu_dram_c5.json)."""
+    import glob
+    paths = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_dram_c5.json")))
+    if not paths:
         return None, None
-    rec = json.load(open(path))
-    return float(rec["dram_bytes_per_attempted_step"]), f"profiles/r01_ncu_dram_c5.json ({rec['kernel']}) x attempted steps"
+    rec = json.load(open(paths[-1]))
+    return (float(rec["dram_bytes_per_attempted_step"]),
+            f"profiles/{os.path.basename(paths[-1])} ({rec['kernel']}) x attempted steps")
 
 
 def run_ours(args):

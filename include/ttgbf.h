@@ -29,6 +29,8 @@
  *   ttgbf_eval_blackbox       the cross black boxes: prior pdf, likelihood,
  *                             FFT kernel, realign evaluator     filters.py:504,697-729,969-979;
  *                                                               models.py:150-153
+ *   ttgbf_rng_draws           numpy Generator.integers / choice as the cross
+ *                             draws them                        tt_algorithms.py:341-433
  *   ttgbf_filter_time_update_std  filters.tt_pmf_step time update (Algorithm 2) filters.py:855-885
  *   ttgbf_dense_*             filters.dense_fft_pmf_step pieces  filters.py:888-934
  *                             (the dense FFT PMF on the GPU)
@@ -350,6 +352,15 @@ int ttgbf_eval_blackbox(int kind, const ttgbf_model* model, const ttgbf_gauss* p
 int ttgbf_negative_mass(const ttgbf_tt* hdr, const double* data, int64_t cap, int count,
                         const ttgbf_axis* axes, int64_t guard, const int32_t* probes, int nprobes,
                         double* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream);
+
+/* The cross's random streams on the device (tt_algorithms.py:341-433 draw
+ * through numpy.random.Generator): kind 0 = rng.integers(0, shape, size=(K, d))
+ * -> out[K*d]; kind 1 = rng.choice(pop, size, replace=False) -> out[size].
+ * state6 (device, in/out): PCG64 state lo/hi, increment lo/hi, has_uint32,
+ * uinteger -- numpy's bit_generator.state after the call equals it.  One CTA;
+ * ws >= 16 * (pop + size) + 2^20 bytes. */
+int ttgbf_rng_draws(int kind, uint64_t* state6, const int32_t* shape, int d, int64_t K, int64_t pop, int64_t size,
+                    int64_t* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream);
 
 /* library info */
 int ttgbf_version(void);

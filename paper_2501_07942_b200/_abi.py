@@ -111,6 +111,7 @@ SIGNATURES = {
     "ttgbf_greedy_cross": [I32, P, P, CrossCfg, P, I32, P, I32, P, P, I64, P, I64, P, P],
     "ttgbf_negative_mass": [P, P, I64, I32, P, I64, P, I32, P, P, I64, P, P],
     "ttgbf_eval_blackbox": [I32, P, P, P, P, P, I64, I32, P, I64, P, P, I64, P, P],
+    "ttgbf_rng_draws": [I32, P, P, I32, I64, I64, I64, P, P, I64, P, P],
     "ttgbf_sizeof": [I32],
     "ttgbf_version": [],
     "ttgbf_block_threads": [],

@@ -375,6 +375,61 @@ int ttgbf_eval_blackbox(int kind, const ttgbf_model* model, const ttgbf_gauss* p
   };
   return launch(count, f, stream);
 }
+
+int ttgbf_rng_draws(int kind, uint64_t* state6, const int32_t* shape, int d, int64_t K, int64_t pop, int64_t size,
+                    int64_t* out, void* ws, int64_t ws_bytes, int32_t* status, void* stream) {
+  auto f = LAMBDA(const Ctx& c, int i, double* smem) {
+    Arena ar = make_arena(ws, ws_bytes, i);
+    XShared* sh = make_stage_smem(smem).xs;
+    double* sm = make_stage_smem(smem).sm;
+    auto body = [&]() -> int {
+      if (c.leader()) {
+        sh->rng.s_lo = state6[0]; sh->rng.s_hi = state6[1]; sh->rng.i_lo = state6[2]; sh->rng.i_hi = state6[3];
+        sh->rng.has32 = (uint32_t)state6[4]; sh->rng.u32 = (uint32_t)state6[5];
+      }
+      c.sync();
+      PcgJump* jt;
+      ALLOC(jt, PcgJump, 1, ar);
+      if (c.leader()) pcg_make_jump(sh->rng, jt);
+      c.sync();
+      if (kind == 0) {
+        int64_t* tmp;
+        int32_t* o32;
+        ALLOC(tmp, int64_t, K * d + 1, ar);
+        ALLOC(o32, int32_t, K * d + 1, ar);
+        warp_integers(c, &sh->rng, jt, shape, d, K, o32, tmp);
+        for (int64_t e = c.tid; e < K * d; e += c.nt) out[e] = o32[e];
+      } else {
+        int32_t* disp;
+        int64_t *touch, *draws;
+        uint8_t* flags;
+        uint32_t* gset;
+        ALLOC(disp, int32_t, pop + 16, ar);
+        ALLOC(touch, int64_t, size + 16, ar);
+        ALLOC(draws, int64_t, size + 16, ar);
+        ALLOC(flags, uint8_t, size + 16, ar);
+        ALLOC(gset, uint32_t, 8 * (size + 16) + 64, ar);
+        par_fill_i32(c, disp, pop + 16, -1);
+        c.sync();
+        warp_choice(c, &sh->rng, jt, pop, size, out, disp, touch, draws, flags, reinterpret_cast<uint32_t*>(sm),
+                    2 * SMEM_SCRATCH_DOUBLES, gset);
+        double bad = 0.0;
+        for (int64_t q = c.tid; q < pop; q += c.nt)
+          if (disp[q] != -1) bad = 1.0;   // the displacement map must be restored
+        if (block_max(c, bad) > 0.0) return E_ARG;
+      }
+      c.sync();
+      if (c.leader()) {
+        state6[0] = sh->rng.s_lo; state6[1] = sh->rng.s_hi; state6[2] = sh->rng.i_lo; state6[3] = sh->rng.i_hi;
+        state6[4] = sh->rng.has32; state6[5] = sh->rng.u32;
+      }
+      return OK;
+    };
+    const int st = body();
+    if (c.leader()) status[i] = st;
+  };
+  return launch(1, f, stream);
+}
 #endif
 
 #if API_PART(1)

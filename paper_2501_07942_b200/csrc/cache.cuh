@@ -37,8 +37,7 @@ struct Cache {
   int64_t count;
   int64_t calls;
   double max_abs;
-  uint64_t tmask;       // current probe-table size - 1 (power of two)
-  uint64_t tmask_max;   // allocated size - 1
+  uint64_t tmask;
   Key* keys;
   double* vals;
   int32_t* table;
@@ -71,41 +70,6 @@ HD int64_t cache_lookup(const Cache& C, const Key& k) {
   }
 }
 
-// Lookup of up to G keys at once: the G probe-table loads are issued
-// together, then the G key loads (each is a DRAM/L2 round trip; one by one
-// they would serialise 2 G latencies).  Collisions continue one at a time.
-template <int G>
-HD void cache_lookup_group(const Cache& C, const Key* k, int g, int64_t* out) {
-  uint64_t h[G];
-  int32_t e[G];
-  Key kk[G];
-#pragma unroll
-  for (int u = 0; u < G; ++u) h[u] = u < g ? (mix64(k[u].hi ^ mix64(k[u].lo)) & C.tmask) : 0;
-#pragma unroll
-  for (int u = 0; u < G; ++u) e[u] = u < g ? C.table[h[u]] : -1;
-#pragma unroll
-  for (int u = 0; u < G; ++u) kk[u] = e[u] >= 0 ? C.keys[e[u]] : Key{0, 0};
-#pragma unroll
-  for (int u = 0; u < G; ++u) {
-    if (u >= g) continue;
-    int64_t r = -1;
-    if (e[u] >= 0) {
-      if (key_eq(kk[u], k[u])) {
-        r = e[u];
-      } else {
-        uint64_t hh = (h[u] + 1) & C.tmask;
-        while (true) {
-          const int32_t e2 = C.table[hh];
-          if (e2 < 0) break;
-          if (key_eq(C.keys[e2], k[u])) { r = e2; break; }
-          hh = (hh + 1) & C.tmask;
-        }
-      }
-    }
-    out[u] = r;
-  }
-}
-
 HD void cache_insert(Cache& C, const Key& k, int32_t e) {
   uint64_t h = mix64(k.hi ^ mix64(k.lo)) & C.tmask;
   while (true) {
@@ -117,23 +81,6 @@ HD void cache_insert(Cache& C, const Key& k, int32_t e) {
 #endif
     h = (h + 1) & C.tmask;
   }
-}
-
-constexpr uint64_t CACHE_TABLE_MIN = 1ull << 16;   // initial probe-table slots
-
-// Grow the probe table (doubling, re-inserting every stored key) until
-// `need` entries load it to at most one half.  All threads call it.
-HDN void cache_reserve(const Ctx& c, Cache* C, int64_t need) {
-  uint64_t tsz = C->tmask + 1;
-  if ((uint64_t)(2 * need) <= tsz || tsz > C->tmask_max) return;
-  while (tsz < (uint64_t)(2 * need) && tsz <= C->tmask_max) tsz <<= 1;
-  c.sync();   // every thread has read the old size
-  par_fill_i32(c, C->table, (int64_t)tsz, -1);
-  if (c.leader()) C->tmask = tsz - 1;
-  c.sync();
-  const int64_t cnt = C->count;
-  for (int64_t e = c.tid; e < cnt; e += c.nt) cache_insert(*C, C->keys[e], (int32_t)e);
-  c.sync();
 }
 
 // Allocate and clear a cache for `cap` entries.
@@ -152,15 +99,8 @@ HDN int cache_init(const Ctx& c, Arena& ar, Cache*& C, int d, const int* n, int6
   ALLOC(keys, Key, cap, ar);
   ALLOC(vals, double, cap, ar);
   ALLOC(table, int32_t, tsz, ar);
-  // The probe table starts small and doubles as the cache fills
-  // (cache_reserve): a cross that evaluates 15k cells probes a 256 KB table
-  // that stays in L2 instead of 8 MB of mostly empty slots, and only the
-  // part in use is ever cleared.
-  const uint64_t tsz_max = tsz;
-  tsz = tsz < CACHE_TABLE_MIN ? tsz : CACHE_TABLE_MIN;
   par_fill_i32(c, table, (int64_t)tsz, -1);
   if (c.leader()) {
-    C->tmask_max = tsz_max - 1;
     C->d = d;
     C->bits = bits;
     for (int k = 0; k < d; ++k) C->n[k] = n[k];
@@ -242,19 +182,11 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
   const int64_t chunk = (K + c.nt - 1) / c.nt;
   const int64_t lo = lmin(K, (int64_t)c.tid * chunk), hi = lmin(K, lo + chunk);
   int64_t nmiss = 0;
-  for (int64_t p = lo; p < hi; p += 4) {
-    const int g = (int)lmin(4, hi - p);
-    Key k4[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) k4[u] = u < g ? pack_key(d, bits, idx + (p + u) * d) : Key{0, 0};
-    int64_t e4[4];
-    cache_lookup_group<4>(*C, k4, g, e4);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (u < g) {
-        pos[p + u] = e4[u];
-        if (e4[u] < 0) ++nmiss;
-      }
+  for (int64_t p = lo; p < hi; ++p) {
+    const Key k = pack_key(d, bits, idx + p * d);
+    const int64_t e = cache_lookup(*C, k);
+    pos[p] = e;
+    if (e < 0) ++nmiss;
   }
   int64_t total;
   int64_t off = scan_offsets(c, nmiss, &total);
@@ -331,7 +263,6 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
     fprintf(stderr, "EV K=%lld M=%lld\n", (long long)K, (long long)M);
 #endif
     if (base + M > C->cap) { ar.release(mk); return E_CACHE; }
-    cache_reserve(c, C, base + M);
     for (int64_t i = lo2; i < hi2; ++i)
       if (i == 0 || !key_eq(sk[i], sk[i - 1])) C->keys[base + (o2++)] = sk[i];
     c.sync();
@@ -371,21 +302,8 @@ HDN int cache_eval(const Ctx& c, Arena& ar, Cache* C, const EvalSpec& spec, cons
       if (M > 0) C->max_abs = fmax(C->max_abs, vmax);
     }
     c.sync();
-    for (int64_t p = lo; p < hi; p += 4) {
-      const int g = (int)lmin(4, hi - p);
-      bool any = false;
-#pragma unroll
-      for (int u = 0; u < 4; ++u) any = any || (u < g && pos[p + u] < 0);
-      if (!any) continue;
-      Key k4[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) k4[u] = u < g ? pack_key(d, bits, idx + (p + u) * d) : Key{0, 0};
-      int64_t e4[4];
-      cache_lookup_group<4>(*C, k4, g, e4);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (u < g && pos[p + u] < 0) pos[p + u] = e4[u];
-    }
+    for (int64_t p = lo; p < hi; ++p)
+      if (pos[p] < 0) pos[p] = cache_lookup(*C, pack_key(d, bits, idx + p * d));
   }
   for (int64_t p = lo; p < hi; ++p) out[p] = C->vals[pos[p]];
   c.sync();

@@ -934,7 +934,9 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
   // per right-hand side: y = Q^T b; triangular / min-norm solve; permute
   for (int q = c.tid; q < nrhs; q += c.nt) {
     // one private vector per thread, solved in place (y -> solution): half
-    // the local-memory footprint of separate y / solution arrays
+    // the local-memory footprint of separate y / solution arrays.  (A fully
+    // unrolled register-resident variant was measured slower: ~10k
+    // instructions per right-hand side thrash the instruction cache.)
     double yy[X_MAXR_SOLVE];
     double* sol = yy;
     for (int i = 0; i < r; ++i) yy[i] = B[i + (int64_t)q * ldb] * bscl;

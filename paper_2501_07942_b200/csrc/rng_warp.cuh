@@ -373,44 +373,114 @@ HDN void warp_choice(const Ctx& c, Pcg64* g, const PcgJump* jt, int64_t pop, int
     out[t] = (int64_t)v;
   }
   c.sync();
-  // in-order resolution of the rare steps: collided[t] lives in flags bit 0.
-  // Warp 0 finds the flagged steps 32 at a time (ballot); the leader
-  // resolves them in order (each may depend on earlier ones).
-  auto resolve = [&](int64_t t) {
-    const uint32_t v = (uint32_t)draws[t];
-    uint64_t h = v & mask;
-    while (keys[h] != v) h = (h + 1) & mask;
-    bool coll = mins[h] < (uint32_t)t;
-    if (!coll && (int64_t)v >= jlo) {
+  // Floyd's collisions: step t collides when its value was drawn before, or
+  // when the value is the j of an earlier step that itself collided (and so
+  // inserted its j).  That chain only walks to smaller t over read-only data,
+  // so every flagged step resolves itself independently.
+  for (int64_t t = c.tid; t < size; t += c.nt) {
+    if (!(flags[t] & 2)) continue;
+    int64_t cur = t;
+    bool coll = false;
+    while (true) {
+      const uint32_t v = (uint32_t)draws[cur];
+      uint64_t h = v & mask;
+      while (keys[h] != v) h = (h + 1) & mask;
+      if (mins[h] < (uint32_t)cur) { coll = true; break; }
+      if ((int64_t)v < jlo) break;
       const int64_t sidx = (int64_t)v - jlo;
-      coll = sidx < t && (flags[sidx] & 1);
+      if (sidx >= cur) break;
+      cur = sidx;
     }
-    if (coll) {
-      out[t] = jlo + t;
-      flags[t] |= 1;
-    }
-  };
-#if ENGINE_DEVICE
-  if (c.tid < 32) {
-    for (int64_t t0 = 0; t0 < size; t0 += 32) {
-      const int64_t t = t0 + c.tid;
-      unsigned mk = __ballot_sync(0xffffffffu, t < size && (flags[t] & 2));
-      if (c.leader()) {
-        while (mk) {
-          const int b = __ffs(mk) - 1;
-          mk &= mk - 1;
-          resolve(t0 + b);
-        }
-      }
-      __syncwarp();
-    }
+    if (coll) out[t] = jlo + t;
   }
-#else
-  for (int64_t t = 0; t < size; ++t)
-    if (flags[t] & 2) resolve(t);
-#endif
   c.sync();
   // Fisher-Yates shuffle of out[0..size): step q swaps i = size-1-q and j = sdraws[q]
+#if ENGINE_DEVICE
+  if (size >= 64 && size <= 4096 && 2 * size + (size + 1) / 2 <= sset_words32) {
+    // All steps at once.  Position i_q is final after step q and receives
+    // V(j_q, q), the value at j_q just before step q.  A position p is
+    // written before its own step only by the steps that drew j = p, each
+    // moving A(q') = V(i_q', q') there; so with the writers of every position
+    // listed in step order,
+    //   A(q) = A(latest q' < q with j_q' = i_q)   or out[i_q] if none,
+    //   F(q) = A(q) if j_q = i_q, else A(latest q' < q with j_q' = j_q) or out[j_q].
+    // The chains only walk to earlier steps (short: a position is drawn
+    // ~ln(size/i) times).
+    const int ns = (int)size - 1;
+    int* cnt = reinterpret_cast<int*>(sset);       // writers per position, then fill cursor
+    int* start = cnt + size;                       // list offsets
+    uint16_t* list = reinterpret_cast<uint16_t*>(start + size);   // writer steps by position, ascending
+    for (int pq = c.tid; pq < (int)size; pq += c.nt) cnt[pq] = 0;
+    c.sync();
+    for (int q = c.tid; q < ns; q += c.nt) atomicAdd(&cnt[(int)sdraws[q]], 1);
+    c.sync();
+    {
+      const int chunk = ((int)size + c.nt - 1) / c.nt;
+      const int p0 = imin((int)size, chunk * c.tid), p1 = imin((int)size, p0 + chunk);
+      int64_t mine = 0;
+      for (int pq = p0; pq < p1; ++pq) mine += cnt[pq];
+      int64_t tot;
+      int64_t off = scan_offsets(c, mine, &tot);
+      for (int pq = p0; pq < p1; ++pq) {
+        start[pq] = (int)off;
+        off += cnt[pq];
+        cnt[pq] = 0;
+      }
+    }
+    c.sync();
+    for (int q = c.tid; q < ns; q += c.nt) {
+      const int j = (int)sdraws[q];
+      list[start[j] + atomicAdd(&cnt[j], 1)] = (uint16_t)q;
+    }
+    c.sync();
+    for (int pq = c.tid; pq < (int)size; pq += c.nt) {
+      const int nq = cnt[pq];
+      uint16_t* l = list + start[pq];
+      for (int a = 1; a < nq; ++a) {   // insertion sort (lists of 1-3 steps)
+        const uint16_t x = l[a];
+        int b2 = a - 1;
+        while (b2 >= 0 && l[b2] > x) { l[b2 + 1] = l[b2]; --b2; }
+        l[b2 + 1] = x;
+      }
+    }
+    c.sync();
+    auto latest = [&](int pq, int q) -> int {   // latest writer of position pq before step q
+      const uint16_t* l = list + start[pq];
+      for (int k = cnt[pq] - 1; k >= 0; --k)
+        if ((int)l[k] < q) return (int)l[k];
+      return -1;
+    };
+    auto before = [&](int q) -> int64_t {       // A(q) = V(i_q, q)
+      int x = q;
+      while (true) {
+        const int pa = latest((int)size - 1 - x, x);
+        if (pa < 0) break;
+        x = pa;
+      }
+      return out[size - 1 - x];
+    };
+    for (int q = c.tid; q <= ns; q += c.nt) {
+      int64_t f;
+      if (q == ns) {                            // position 0 is never an i: its last writer decides
+        const int pf = latest(0, ns);
+        f = pf >= 0 ? before(pf) : out[0];
+      } else {
+        const int i = (int)size - 1 - q, j = (int)sdraws[q];
+        if (j == i) {
+          f = before(q);
+        } else {
+          const int pf = latest(j, q);
+          f = pf >= 0 ? before(pf) : out[j];
+        }
+      }
+      draws[q] = f;
+    }
+    c.sync();
+    for (int q = c.tid; q <= ns; q += c.nt) out[q == ns ? 0 : size - 1 - q] = draws[q];
+    c.sync();
+    return;
+  }
+#endif
   swap_resolve(
       c, size > 1 ? size - 1 : 0, [=](int64_t q) { return size - 1 - q; }, [=](int64_t q) { return sdraws[q]; },
       [=](int64_t pos) { return out[pos]; }, [=](int64_t pos, int64_t v) { out[pos] = v; },

@@ -843,6 +843,51 @@ __device__ __forceinline__ void rrqr_update_cols(double* A, int m, int n, int j,
 }
 #endif
 
+#if ENGINE_DEVICE
+// Register-resident form of rrqr_update_cols for columns of at most 32 * RL
+// rows below the pivot: a warp loads its column once (all loads in flight),
+// forms the dot product, updates and stores it and takes the new norm from
+// the registers -- one read and one write of the trailing block per pivot
+// step instead of two reads and a write.  Same per-lane accumulation order
+// and shuffle tree as rrqr_update_cols, so the values are identical.
+template <int RL>
+__device__ __noinline__ void rrqr_update_cols_reg(double* A, int m, int n, int j, const double* col, double t,
+                                                  double* cn, int warp, int nwarps, int lane) {
+  // the reflector is re-read per column (10 KB, L1-resident, shared by the
+  // warps): only the column itself is held in registers
+  auto vat = [&](int r) { return r == j ? 1.0 : col[r]; };
+  for (int qc = j + 1 + warp; qc < n; qc += nwarps) {
+    double* cq = A + (int64_t)qc * m;
+    double x[RL];
+#pragma unroll
+    for (int q = 0; q < RL; ++q) {
+      const int r = j + lane + 32 * q;
+      x[q] = r < m ? cq[r] : 0.0;
+    }
+    double w = 0.0;
+#pragma unroll
+    for (int q = 0; q < RL; ++q) {
+      const int r = j + lane + 32 * q;
+      if (r < m) w = fma(vat(r), x[q], w);
+    }
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    w *= t;
+    double nr = 0.0;
+#pragma unroll
+    for (int q = 0; q < RL; ++q) {
+      const int r = j + lane + 32 * q;
+      if (r < m) {
+        const double y = x[q] - w * vat(r);
+        cq[r] = y;
+        if (r > j) nr = fma(y, y, nr);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) nr += __shfl_xor_sync(0xffffffffu, nr, o);
+    if (lane == 0) cn[qc] = nr;
+  }
+}
+#endif
+
 HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double eps_abs, double** U_out,
                  double** s_out, double** Vt_out, int* kk_out, double* sm, int want = 0) {
   PROF(c, 8);
@@ -930,7 +975,12 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
     // flight per lane; every column keeps its own accumulation order, so the
     // values are those of the one-column-per-warp loop
     const int ntr = n - j - 1;
-    if (ntr >= 8 * nwarps) rrqr_update_cols<4>(A, m, n, j, col, t, cn, warp, nwarps, lane);
+    const int rl = (m - j + 31) / 32;
+    if (rl <= 8) rrqr_update_cols_reg<8>(A, m, n, j, col, t, cn, warp, nwarps, lane);
+    else if (rl <= 16) rrqr_update_cols_reg<16>(A, m, n, j, col, t, cn, warp, nwarps, lane);
+    else if (rl <= 28) rrqr_update_cols_reg<28>(A, m, n, j, col, t, cn, warp, nwarps, lane);
+    else if (rl <= 42) rrqr_update_cols_reg<42>(A, m, n, j, col, t, cn, warp, nwarps, lane);
+    else if (ntr >= 8 * nwarps) rrqr_update_cols<4>(A, m, n, j, col, t, cn, warp, nwarps, lane);
     else if (ntr >= 2 * nwarps) rrqr_update_cols<2>(A, m, n, j, col, t, cn, warp, nwarps, lane);
     else rrqr_update_cols<1>(A, m, n, j, col, t, cn, warp, nwarps, lane);
 #else

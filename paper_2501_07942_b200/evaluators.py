@@ -115,3 +115,35 @@ def realign_values(model, conv_tt, filt_grid, pred_grid, idx) -> np.ndarray:
     """The convolved TT (on ``filt_grid``) at F^-1 y for predictive nodes y
     (the realign black box of tt_fft_pmf_step); zero outside the hull."""
     return _call(_abi.BB_REALIGN, _spec(model), idx, tt=conv_tt, filt=filt_grid, pred=pred_grid)
+
+
+def rng_draws(state6, *, shape=None, K=0, pop=0, size=0):
+    """The cross's numpy-compatible draws on the device (``ttgbf_rng_draws``).
+
+    ``state6`` is numpy's PCG64 state as six uint64 (state lo/hi, increment
+    lo/hi, has_uint32, uinteger).  With ``shape``: ``rng.integers(0, shape,
+    size=(K, len(shape)))``; otherwise ``rng.choice(pop, size, replace=False)``.
+    Returns (values, state6 after the call)."""
+    from paper_2501_07942_b200.tensor_train import _be
+    be = _be()
+    st = be.upload(np.asarray(state6, dtype=np.uint64))
+    status = be.upload(np.zeros(1, dtype=np.int32))
+    if shape is not None:
+        sh = np.asarray(shape, dtype=np.int32)
+        n, kind = int(K) * sh.size, 0
+        shd = be.upload(sh)
+        d = sh.size
+    else:
+        n, kind = int(size), 1
+        shd = be.upload(np.zeros(1, dtype=np.int32))
+        d = 1
+    out = be.empty(8 * max(n, 1))
+    ws_bytes = 16 * (int(pop) + 8 * int(size) + int(K) * d) + (1 << 20)
+    ws = be.empty(ws_bytes)
+    be.check(be.lib.ttgbf_rng_draws(kind, st.ptr, shd.ptr, d, int(K), int(pop), int(size), out.ptr, ws.ptr, ws_bytes,
+                                    status.ptr, be.stream_ptr), "ttgbf_rng_draws")
+    be.sync()
+    rc = int(be.download(status, np.int32, 1)[0])
+    if rc != 0:
+        raise RuntimeError(f"ttgbf_rng_draws: {_abi.status_text(rc)}")
+    return be.download(out, np.int64, n), be.download(st, np.uint64, 6)

@@ -58,3 +58,46 @@ def test_choice_matches_numpy(lib, pop, size):
         ref = rng.choice(pop, size=size, replace=False)
         assert np.array_equal(got, ref)
         assert np.array_equal(st, state_of(rng))
+
+
+# -- the same streams through the C-ABI entry ttgbf_rng_draws: host emulation
+# (CPU suite) and the sm_100a kernel itself (-m gpu), where the draws are
+# warp-parallel, the tail-shuffle steps are resolved by all threads and only
+# the interacting ones replayed in order
+CHOICES = [(33, 10), (2600, 1024), (5000, 1024), (9999, 4096), (10001, 1024), (20000, 4096), (60000, 4096),
+           (300000, 4096), (150000, 32768), (12000, 8192), (1030, 1024), (4097, 4096), (1000000, 32768), (900, 700)]
+
+
+def check_abi_draws():
+    from paper_2501_07942_b200 import evaluators as ev
+    for seed in range(2):
+        rng = np.random.default_rng(seed)
+        rng.integers(0, 7)
+        for shape, K in [((65,) * 6, 56), ((33, 129, 7), 300)]:
+            got, st = ev.rng_draws(state_of(rng), shape=shape, K=K)
+            ref = rng.integers(0, shape, size=(K, len(shape)))
+            assert np.array_equal(got.reshape(K, -1), ref), (shape, K)
+            assert np.array_equal(st, state_of(rng))
+        for pop, size in CHOICES:
+            got, st = ev.rng_draws(state_of(rng), pop=pop, size=size)
+            ref = rng.choice(pop, size=size, replace=False)
+            assert np.array_equal(got, ref), (pop, size, int((got != ref).sum()))
+            assert np.array_equal(st, state_of(rng)), (pop, size)
+
+
+def test_abi_draws_hostsim():
+    from hostsim import HostBackend
+    from scenario_util import use_backend
+    use_backend(HostBackend())
+    check_abi_draws()
+
+
+@pytest.mark.gpu
+def test_abi_draws_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test run without a CUDA device")
+    from paper_2501_07942_b200.backend import CudaBackend
+    from scenario_util import use_backend
+    use_backend(CudaBackend())
+    check_abi_draws()
