@@ -442,6 +442,7 @@ def run_ours(args):
         "device_busy_frac": kern_total / dev_s if dev_s > 0 else None,
         "stage_cycles_share": (stats["cycles"] / max(stats["cycles"].sum(), 1)).round(4).tolist(),
         "engine_prof_share": dict(zip(PROF_NAMES, (stats["prof"][:22] / max(stats["cycles"].sum(), 1)).round(4).tolist())),
+        "lstsq_factor_share": round(float(stats["prof"][31] / max(stats["cycles"].sum(), 1)), 4),
         "squeeze_share": round(float(stats["prof"][30] / max(stats["cycles"].sum(), 1)), 4),
         "svd_rrqr_mean_rank": float(stats["prof"][22] / max(stats["prof"][23], 1)),
         "svd_detail": {"max_rank": int(dg["prof"][:, 24].max()),

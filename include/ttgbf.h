@@ -136,7 +136,7 @@ typedef struct {
    * 15 negative mass, 16 qr panel, 17 qr trailing update, 18 round R-multiply,
    * 19 round apply_q, 20 fft spectra+product, 21 svd rrqr, 22 rrqr rank sum (count, not cycles), 23 svd_rrqr calls,
    * 24 max rrqr rank (count), 25 svd jacobi, 26 svd U from reflectors, 27 svd Bt QR + V,
-   * 28 svd calls with rank > 64 (count), 29 their cycles, 30 exact-rank squeeze of cross outputs, 31 spare */
+   * 28 svd calls with rank > 64 (count), 29 their cycles, 30 exact-rank squeeze of cross outputs, 31 core-solve factorisation (within 3) */
   int64_t prof[32];
   int64_t big_used;       /* steps that borrowed an overflow workspace */
   int64_t big_peak;       /* peak bytes used in an overflow workspace */

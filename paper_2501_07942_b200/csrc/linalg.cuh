@@ -760,6 +760,7 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
   }
   for (int j = c.tid; j < r; j += c.nt) jpvt[j] = j;
   c.sync();
+  const int64_t t_fact = clk();
 #if ENGINE_DEVICE
   const bool w0 = c.tid < 32;
   const int lane = c.tid & 31, L = 32;
@@ -917,6 +918,7 @@ HDN int lstsq_pivoted(const Ctx& c, const double* A, int64_t lda_r, int64_t lda_
   }
 #undef WSYNC
   c.sync();
+  if (c.prof && c.leader()) c.prof[31] += clk() - t_fact;   // factorisation + rank (warp 0), the rest is the solve phase
   const int rank = c.ired[0];
   if (rank_out) *rank_out = rank;
   // dgelsy's scaling of B into [smlnum, bignum] (one factor for all of B)
