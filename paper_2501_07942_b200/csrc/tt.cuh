@@ -433,6 +433,7 @@ struct PtsFn {
 // ---------------------------------------------------------------------------
 constexpr int64_t BUCKET_MIN_K = 64;
 constexpr int BUCKET_MAXR = 160;
+constexpr int EVAL_TILE = 16;   // points per warp tile of the bucketed evaluation
 
 template <class Slice>
 HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice slice, double* out, double* sm) {
@@ -504,7 +505,7 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
         toffs[q] = tacc;
         cur[q] = acc;
         acc += h;
-        tacc += (h + 7) >> 3;
+        tacc += (h + EVAL_TILE - 1) / EVAL_TILE;
       }
       offs[n] = acc;
       toffs[n] = tacc;
@@ -535,42 +536,61 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
           if (toffs[mid] <= tile) lo_ = mid; else hi_ = mid;
         }
         const int sl = lo_;
-        const int q0 = offs[sl] + 8 * (tile - toffs[sl]);
+        // 16 points of one slice per tile: every B fragment (a 4 x 8 piece of
+        // the slice, the load the loop waits on) feeds two A fragments
+        const int q0 = offs[sl] + EVAL_TILE * (tile - toffs[sl]);
         const int end = offs[sl + 1];
-        const int qa = q0 + ar_;
-        const bool rv = qa < end;
-        const int pa = perm[rv ? qa : q0];
-        const double* vrow = Vin + (int64_t)pa * maxr;
-        const double wl = wlv[pa], wh = whv[pa];
+        const int qa = q0 + ar_, qb = q0 + 8 + ar_;
+        const bool rva = qa < end, rvb = qb < end;
+        const int pa = perm[rva ? qa : q0], pb = perm[rvb ? qb : q0];
+        const double* vra = Vin + (int64_t)pa * maxr;
+        const double* vrb = Vin + (int64_t)pb * maxr;
+        const double wla = wlv[pa], wha = whv[pa], wlb = wlv[pb], whb = whv[pb];
         const double* Gs = G + (int64_t)sl * rr;
         const bool has_hi = sl + 1 < n;
         for (int n0 = 0; n0 < rr; n0 += 8) {
           double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+          double d0 = 0.0, d1 = 0.0, f0 = 0.0, f1 = 0.0;
           const int bcol = n0 + ar_;
 #pragma unroll 4
           for (int k0 = 0; k0 < rl; k0 += 4) {
             const int ka = k0 + ac;
-            const double af = (rv && ka < rl) ? vrow[ka] : 0.0;
+            const double afa = (rva && ka < rl) ? vra[ka] : 0.0;
+            const double afb = (rvb && ka < rl) ? vrb[ka] : 0.0;
             const bool bv = ka < rl && bcol < rr;
             const double* gp = Gs + (int64_t)ka * sa + bcol;
             const double bf = bv ? gp[0] : 0.0;
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                         : "+d"(c0), "+d"(c1) : "d"(af), "d"(bf));
+                         : "+d"(c0), "+d"(c1) : "d"(afa), "d"(bf));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(d0), "+d"(d1) : "d"(afb), "d"(bf));
             if (Slice::kBlend) {
               const double bf2 = (bv && has_hi) ? gp[rr] : 0.0;
               asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                           : "+d"(e0), "+d"(e1) : "d"(af), "d"(bf2));
+                           : "+d"(e0), "+d"(e1) : "d"(afa), "d"(bf2));
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                           : "+d"(f0), "+d"(f1) : "d"(afb), "d"(bf2));
             }
           }
-          if (rv) {
-            const int oc = n0 + 2 * ac;
+          const int oc = n0 + 2 * ac;
+          if (rva) {
             double* orow = Vout + (int64_t)pa * maxr;
             if (Slice::kBlend) {
-              if (oc < rr) orow[oc] = c0 * wl + e0 * wh;
-              if (oc + 1 < rr) orow[oc + 1] = c1 * wl + e1 * wh;
+              if (oc < rr) orow[oc] = c0 * wla + e0 * wha;
+              if (oc + 1 < rr) orow[oc + 1] = c1 * wla + e1 * wha;
             } else {
               if (oc < rr) orow[oc] = c0;
               if (oc + 1 < rr) orow[oc + 1] = c1;
+            }
+          }
+          if (rvb) {
+            double* orow = Vout + (int64_t)pb * maxr;
+            if (Slice::kBlend) {
+              if (oc < rr) orow[oc] = d0 * wlb + f0 * whb;
+              if (oc + 1 < rr) orow[oc + 1] = d1 * wlb + f1 * whb;
+            } else {
+              if (oc < rr) orow[oc] = d0;
+              if (oc + 1 < rr) orow[oc + 1] = d1;
             }
           }
         }
