@@ -433,7 +433,10 @@ struct PtsFn {
 // ---------------------------------------------------------------------------
 constexpr int64_t BUCKET_MIN_K = 64;
 constexpr int BUCKET_MAXR = 160;
-constexpr int EVAL_TILE = 16;   // points per warp tile of the bucketed evaluation
+#ifndef TTGBF_EVAL_TILE
+#define TTGBF_EVAL_TILE 16
+#endif
+constexpr int EVAL_TILE = TTGBF_EVAL_TILE;   // points per warp tile of the bucketed evaluation
 
 template <class Slice>
 HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice slice, double* out, double* sm) {
@@ -536,61 +539,64 @@ HDN int tt_eval_bucketed(const Ctx& c, Arena& ar, const TT& t, int64_t K, Slice 
           if (toffs[mid] <= tile) lo_ = mid; else hi_ = mid;
         }
         const int sl = lo_;
-        // 16 points of one slice per tile: every B fragment (a 4 x 8 piece of
-        // the slice, the load the loop waits on) feeds two A fragments
+        // EVAL_TILE points of one slice per tile: every B fragment (a 4 x 8
+        // piece of the slice, the load the loop waits on) feeds EVAL_TILE / 8
+        // A fragments
+        constexpr int NA = EVAL_TILE / 8;
         const int q0 = offs[sl] + EVAL_TILE * (tile - toffs[sl]);
         const int end = offs[sl + 1];
-        const int qa = q0 + ar_, qb = q0 + 8 + ar_;
-        const bool rva = qa < end, rvb = qb < end;
-        const int pa = perm[rva ? qa : q0], pb = perm[rvb ? qb : q0];
-        const double* vra = Vin + (int64_t)pa * maxr;
-        const double* vrb = Vin + (int64_t)pb * maxr;
-        const double wla = wlv[pa], wha = whv[pa], wlb = wlv[pb], whb = whv[pb];
+        bool rv[NA];
+        int pp[NA];
+        const double* vr[NA];
+        double wl[NA], wh[NA];
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+          const int qa = q0 + 8 * a + ar_;
+          rv[a] = qa < end;
+          pp[a] = perm[rv[a] ? qa : q0];
+          vr[a] = Vin + (int64_t)pp[a] * maxr;
+          wl[a] = wlv[pp[a]];
+          wh[a] = whv[pp[a]];
+        }
         const double* Gs = G + (int64_t)sl * rr;
         const bool has_hi = sl + 1 < n;
         for (int n0 = 0; n0 < rr; n0 += 8) {
-          double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
-          double d0 = 0.0, d1 = 0.0, f0 = 0.0, f1 = 0.0;
+          double cc[NA][2], ee[NA][2];
+#pragma unroll
+          for (int a = 0; a < NA; ++a) cc[a][0] = cc[a][1] = ee[a][0] = ee[a][1] = 0.0;
           const int bcol = n0 + ar_;
 #pragma unroll 4
           for (int k0 = 0; k0 < rl; k0 += 4) {
             const int ka = k0 + ac;
-            const double afa = (rva && ka < rl) ? vra[ka] : 0.0;
-            const double afb = (rvb && ka < rl) ? vrb[ka] : 0.0;
+            double af[NA];
+#pragma unroll
+            for (int a = 0; a < NA; ++a) af[a] = (rv[a] && ka < rl) ? vr[a][ka] : 0.0;
             const bool bv = ka < rl && bcol < rr;
             const double* gp = Gs + (int64_t)ka * sa + bcol;
             const double bf = bv ? gp[0] : 0.0;
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                         : "+d"(c0), "+d"(c1) : "d"(afa), "d"(bf));
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                         : "+d"(d0), "+d"(d1) : "d"(afb), "d"(bf));
+#pragma unroll
+            for (int a = 0; a < NA; ++a)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                           : "+d"(cc[a][0]), "+d"(cc[a][1]) : "d"(af[a]), "d"(bf));
             if (Slice::kBlend) {
               const double bf2 = (bv && has_hi) ? gp[rr] : 0.0;
-              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                           : "+d"(e0), "+d"(e1) : "d"(afa), "d"(bf2));
-              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-                           : "+d"(f0), "+d"(f1) : "d"(afb), "d"(bf2));
+#pragma unroll
+              for (int a = 0; a < NA; ++a)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                             : "+d"(ee[a][0]), "+d"(ee[a][1]) : "d"(af[a]), "d"(bf2));
             }
           }
           const int oc = n0 + 2 * ac;
-          if (rva) {
-            double* orow = Vout + (int64_t)pa * maxr;
+#pragma unroll
+          for (int a = 0; a < NA; ++a) {
+            if (!rv[a]) continue;
+            double* orow = Vout + (int64_t)pp[a] * maxr;
             if (Slice::kBlend) {
-              if (oc < rr) orow[oc] = c0 * wla + e0 * wha;
-              if (oc + 1 < rr) orow[oc + 1] = c1 * wla + e1 * wha;
+              if (oc < rr) orow[oc] = cc[a][0] * wl[a] + ee[a][0] * wh[a];
+              if (oc + 1 < rr) orow[oc + 1] = cc[a][1] * wl[a] + ee[a][1] * wh[a];
             } else {
-              if (oc < rr) orow[oc] = c0;
-              if (oc + 1 < rr) orow[oc + 1] = c1;
-            }
-          }
-          if (rvb) {
-            double* orow = Vout + (int64_t)pb * maxr;
-            if (Slice::kBlend) {
-              if (oc < rr) orow[oc] = d0 * wlb + f0 * whb;
-              if (oc + 1 < rr) orow[oc + 1] = d1 * wlb + f1 * whb;
-            } else {
-              if (oc < rr) orow[oc] = d0;
-              if (oc + 1 < rr) orow[oc + 1] = d1;
+              if (oc < rr) orow[oc] = cc[a][0];
+              if (oc + 1 < rr) orow[oc + 1] = cc[a][1];
             }
           }
         }
