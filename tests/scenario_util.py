@@ -339,3 +339,25 @@ def check_baseline_band(rows, band, min_stable=1):
     assert not bad, bad
     assert n_stable >= min_stable, (n_stable, n_chaotic)
     return {"stable": n_stable, "chaotic": n_chaotic, "chaotic_matched": n_match_chaotic}
+
+
+def check_squeeze_ranks(recs, d, expect_drop):
+    """The exact-rank squeeze of the cross outputs (filter.cuh tt_squeeze): a
+    step record carries the kernel / likelihood ranks as the cross returned
+    them (slots 4 / 1) and as the products used them (slots 9 / 8).  Squeezed
+    ranks never exceed the cross's; with expect_drop (BASELINE C3: the
+    correlated-Q kernel cross is rank deficient) some bond must shrink.
+    Returns the number of bond directions removed."""
+    dropped = 0
+    for r in recs:
+        if int(r["status"]) != 0:
+            continue
+        ranks = r["ranks"]
+        for raw, sq in ((4, 9), (1, 8)):
+            a, b = ranks[raw][: d + 1], ranks[sq][: d + 1]
+            assert int(b[0]) == 1 and int(b[d]) == 1, (raw, b)
+            assert all(int(y) <= int(x) for x, y in zip(a, b)), (raw, a, b)
+            dropped += int(sum(int(x) - int(y) for x, y in zip(a, b)))
+    if expect_drop:
+        assert dropped > 0, "the squeeze removed no direction on a rank-deficient cross output"
+    return dropped

@@ -35,3 +35,16 @@ def test_large_eval_hostsim(golden, backend, case):
     from scenario_util import check_large_eval, use_backend
     use_backend(backend)
     check_large_eval(golden, case)
+
+
+def test_squeeze_ranks_hostsim(golden, backend):
+    """Rank log of the exact-rank squeeze on a golden scenario (full-rank cross
+    outputs there: nothing may grow; the drop itself is asserted on C3, GPU)."""
+    from scenario_util import SCENARIOS, FilterBank, bank_config, check_squeeze_ranks
+    name = "radar_deg"
+    z = golden("trajectories")
+    sc = SCENARIOS[name]
+    bank = FilterBank(sc["spec"], bank_config(sc), 1, backend=backend)
+    done = int(z[f"{name}/done"])
+    recs = bank.run(z[f"{name}/z"][None, :, :], done, sc["x0_mean"], sc["x0_cov"])[0]
+    check_squeeze_ranks(recs[:done], sc["spec"]["F"].shape[0], expect_drop=False)

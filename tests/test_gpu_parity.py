@@ -73,6 +73,22 @@ def test_round_tall_cores_gpu(cuda, ranks, tol):
     assert rel(T.to_full(got.numpy_cores()), T.to_full(ref)) <= 1e-11
 
 
+def test_squeeze_ranks_gpu(golden, cuda):
+    """Exact-rank squeeze of the cross outputs on BASELINE C3 (correlated-Q
+    kernel: its cross output is rank deficient): the ranks the products use
+    are below the cross's on some bond, never above."""
+    import numpy as np
+    from scenario_util import baseline_bank, check_squeeze_ranks
+    z = golden("baseline")
+    cfg, bank = baseline_bank("C3", 4, cuda)
+    Z = np.stack([z[f"C3/{r}/z"] for r in range(4)])
+    recs = bank.run(Z, 1, cfg["x0_mean"], cfg["x0_cov"])
+    d = cfg["spec"]["F"].shape[0]
+    assert (recs["status"][:, 0] == 0).any()
+    dropped = check_squeeze_ranks(recs[:, 0], d, expect_drop=True)
+    print({"squeezed_bond_directions": dropped})
+
+
 @pytest.mark.parametrize("name", ["scaling2_tight", "radar_deg", "identity2", "cv4_step0"])
 def test_persistent_run_gpu(golden, cuda, name):
     """The benchmarked path -- ttgbf_filter_run, one persistent launch with
