@@ -74,6 +74,14 @@ struct ProfScope {
 };
 #define PROF(c, cat) ::tg::ProfScope _prof_##cat((c).prof, (c).tid, cat)
 
+// Quotient / remainder of loop indices: the 32-bit divide when both operands
+// are below 2^31 (the 64-bit one costs ~5x more instructions on the device).
+HD int64_t qdiv(int64_t e, int64_t d) {
+  return ((e | d) >> 31) == 0 ? (int64_t)((unsigned)e / (unsigned)d) : e / d;
+}
+HD int64_t qmod(int64_t e, int64_t d) {
+  return ((e | d) >> 31) == 0 ? (int64_t)((unsigned)e % (unsigned)d) : e % d;
+}
 HD int imin(int a, int b) { return a < b ? a : b; }
 HD int imax(int a, int b) { return a > b ? a : b; }
 HD int64_t lmin(int64_t a, int64_t b) { return a < b ? a : b; }

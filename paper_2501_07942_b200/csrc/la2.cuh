@@ -636,14 +636,10 @@ HDN void qr_panel_ll(const Ctx& c, double* A, int64_t lda, int m, int j0, int jb
 // zeros above) into Vc (col-major, ld = m - j0).
 HD void copy_v(const Ctx& c, const double* A, int64_t lda, int m, int j0, int jb, double* Vc) {
   const int64_t mr = m - j0;
-  for (int64_t e = c.tid; e < mr * jb; e += c.nt) {
-    const int64_t r = e % mr;
-    const int q = (int)(e / mr);
-    double v;
-    if (r < q) v = 0.0;
-    else if (r == q) v = 1.0;
-    else v = A[(int64_t)(j0 + q) * lda + j0 + r];
-    Vc[e] = v;
+  for (int q = 0; q < jb; ++q) {
+    const double* aq = A + (int64_t)(j0 + q) * lda + j0;
+    double* vq = Vc + (int64_t)q * mr;
+    for (int64_t r = c.tid; r < mr; r += c.nt) vq[r] = r < q ? 0.0 : (r == q ? 1.0 : aq[r]);
   }
   c.sync();
 }

@@ -117,7 +117,7 @@ HDN int tt_moments(const Ctx& c, Arena& ar, const TT& t, const double* const* ax
     const int rl = t.r[k], n = t.n[k], rr = t.r[k + 1];
     for (int p = 0; p < 3; ++p) ALLOC(M[k][p], double, (int64_t)rl * rr, ar);
     for (int64_t e = c.tid; e < (int64_t)rl * rr; e += c.nt) {
-      const int a = (int)(e / rr), b = (int)(e % rr);
+      const int a = (int)(qdiv(e, rr)), b = (int)(qmod(e, rr));
       const double* g = t.c[k] + (int64_t)a * n * rr + b;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
       for (int i = 0; i < n; ++i) {
@@ -676,9 +676,9 @@ HDN int tt_interp(const Ctx& c, Arena& ar, const TT& t, const AxisGeom* old_geo,
     const int rl = t.r[k], n = t.n[k], rr = t.r[k + 1];
     const int64_t tot = out.size(k);
     for (int64_t e = c.tid; e < tot; e += c.nt) {
-      const int b = (int)(e % rr);
-      const int j = (int)((e / rr) % n);
-      const int a = (int)(e / ((int64_t)rr * n));
+      const int b = (int)(qmod(e, rr));
+      const int j = (int)(qmod(qdiv(e, rr), n));
+      const int a = (int)(qdiv(e, (int64_t)rr * n));
       int cell;
       double frac;
       bool inside;
@@ -737,7 +737,7 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
   ALLOC(Y, double, (int64_t)yr * yc, ar);
   if (tall) {  // Y = X (col-major copy)
     for (int64_t e = c.tid; e < (int64_t)m * n; e += c.nt) {
-      const int i = (int)(e / n), j = (int)(e % n);
+      const int i = (int)(qdiv(e, n)), j = (int)(qmod(e, n));
       Y[i + (int64_t)j * m] = X[e];
     }
   } else {     // Y = X^T (col-major (n x m)) == X's buffer
@@ -757,7 +757,7 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
     Qy = Y;   // reflectors; Q is applied implicitly below
     ALLOC(Z, double, (int64_t)yc * yc, ar);
     for (int64_t e = c.tid; e < (int64_t)yc * yc; e += c.nt) {
-      const int i = (int)(e % yc), j = (int)(e / yc);
+      const int i = (int)(qmod(e, yc)), j = (int)(qdiv(e, yc));
       Z[e] = (i <= j) ? Y[i + (int64_t)j * yr] : 0.0;
     }
     c.sync();
@@ -772,14 +772,14 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
   if (Qy) {
     // Uy = Q [Z[:, perm]; 0]
     for (int64_t e = c.tid; e < (int64_t)yr * kk; e += c.nt) {
-      const int i = (int)(e % yr), j = (int)(e / yr);
+      const int i = (int)(qmod(e, yr)), j = (int)(qdiv(e, yr));
       Uy[e] = (i < zr) ? Z[i + (int64_t)perm[j] * zr] : 0.0;
     }
     c.sync();
     CK(apply_q(c, ar, Qy, yr, yr, yc, Tq, false, Uy, yr, kk, sm));
   } else {
     for (int64_t e = c.tid; e < (int64_t)yr * kk; e += c.nt) {
-      const int i = (int)(e % yr), j = (int)(e / yr);
+      const int i = (int)(qmod(e, yr)), j = (int)(qdiv(e, yr));
       Uy[e] = Z[i + (int64_t)perm[j] * zr];
     }
     c.sync();
@@ -787,16 +787,16 @@ HDN int svd_rowmajor(const Ctx& c, Arena& ar, const double* X, int m, int n, dou
   if (tall) {  // X = Uy S Vj^T : U = Uy, Vt[j, :] = Vj[:, perm[j]]
     par_copy(c, U, Uy, (int64_t)m * kk);
     for (int64_t e = c.tid; e < (int64_t)kk * n; e += c.nt) {
-      const int j = (int)(e / n), q = (int)(e % n);
+      const int j = (int)(qdiv(e, n)), q = (int)(qmod(e, n));
       Vt[e] = Vj[q + (int64_t)perm[j] * yc];
     }
   } else {     // X^T = Uy S Vj^T -> X = Vj S Uy^T : U = Vj[:, perm], Vt = Uy^T
     for (int64_t e = c.tid; e < (int64_t)m * kk; e += c.nt) {
-      const int i = (int)(e % m), j = (int)(e / m);
+      const int i = (int)(qmod(e, m)), j = (int)(qdiv(e, m));
       U[e] = Vj[i + (int64_t)perm[j] * yc];
     }
     for (int64_t e = c.tid; e < (int64_t)kk * n; e += c.nt) {
-      const int j = (int)(e / n), q = (int)(e % n);
+      const int j = (int)(qdiv(e, n)), q = (int)(qmod(e, n));
       Vt[e] = Uy[q + (int64_t)j * yr];
     }
   }
@@ -931,7 +931,7 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
   ALLOC(tau, double, kmax, ar);
   ALLOC(perm, int, n, ar);
   for (int64_t e = c.tid; e < (int64_t)m * n; e += c.nt) {
-    const int i = (int)(e / n), j = (int)(e % n);
+    const int i = (int)(qdiv(e, n)), j = (int)(qmod(e, n));
     A[i + (int64_t)j * m] = X[e];
   }
   for (int j = c.tid; j < n; j += c.nt) perm[j] = j;
@@ -1053,7 +1053,7 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
   int* jp;
   ALLOC(Bt, double, (int64_t)n * p, ar);
   for (int64_t e = c.tid; e < (int64_t)n * p; e += c.nt) {
-    const int q = (int)(e % n), i = (int)(e / n);
+    const int q = (int)(qmod(e, n)), i = (int)(qdiv(e, n));
     Bt[perm[q] + (int64_t)i * n] = (i <= q) ? A[i + (int64_t)q * m] : 0.0;
   }
   c.sync();
@@ -1065,7 +1065,7 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
   // R2^T Vj = Uz S  =>  B = R2^T Q2^T = Uz S (Q2 Vj)^T
   ALLOC(Z, double, (int64_t)p * p, ar);
   for (int64_t e = c.tid; e < (int64_t)p * p; e += c.nt) {
-    const int i = (int)(e % p), j = (int)(e / p);     // Z(i, j) = R2(j, i)
+    const int i = (int)(qmod(e, p)), j = (int)(qdiv(e, p));     // Z(i, j) = R2(j, i)
     Z[e] = (j <= i) ? Bt[j + (int64_t)i * n] : 0.0;
   }
   ALLOC(tmp, double, p, ar);
@@ -1091,14 +1091,14 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
     else jacobi_cols_reg<32>(c, Z, p, p, p);
     jacobi_finish(c, Z, p, p, p, s, jp, tmp);
     for (int64_t e = c.tid; e < (int64_t)p * nw; e += c.nt) {
-      const int i = (int)(e % p), j = (int)(e / p);
+      const int i = (int)(qmod(e, p)), j = (int)(qdiv(e, p));
       Uz[e] = Z[i + (int64_t)jp[j] * p];
     }
     c.sync();
     // Vw(0:p, j) = Z0^T Uz(:, j) / s_j
     gemm_dm<32>(c, p, nw, p, 1.0, Mat{Z0, p, 1}, Mat{Uz, 1, p}, 0.0, Vw, 1, n, sm);
     for (int64_t e = c.tid; e < (int64_t)n * nw; e += c.nt) {
-      const int i = (int)(e % n), j = (int)(e / n);
+      const int i = (int)(qmod(e, n)), j = (int)(qdiv(e, n));
       if (i >= p) Vw[e] = 0.0;
       else Vw[e] = s[j] > 0.0 ? Vw[e] / s[j] : 0.0;
     }
@@ -1111,11 +1111,11 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
     ALLOC(Vj, double, (int64_t)p * p, ar);
     CK(svd_jacobi(c, Z, p, p, p, Vj, s, jp, tmp));
     for (int64_t e = c.tid; e < (int64_t)p * nw; e += c.nt) {
-      const int i = (int)(e % p), j = (int)(e / p);
+      const int i = (int)(qmod(e, p)), j = (int)(qdiv(e, p));
       Uz[e] = Z[i + (int64_t)jp[j] * p];
     }
     for (int64_t e = c.tid; e < (int64_t)n * nw; e += c.nt) {
-      const int i = (int)(e % n), j = (int)(e / n);
+      const int i = (int)(qmod(e, n)), j = (int)(qdiv(e, n));
       Vw[e] = (i < p) ? Vj[i + (int64_t)jp[j] * p] : 0.0;
     }
     c.sync();
@@ -1123,7 +1123,7 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
   sec(25);
   // U = Q1 [Uz; 0]   (m x nw);  Q1 = H_0 .. H_{p-1} of the pivoted QR
   for (int64_t e = c.tid; e < (int64_t)m * nw; e += c.nt) {
-    const int i = (int)(e % m), j = (int)(e / m);
+    const int i = (int)(qmod(e, m)), j = (int)(qdiv(e, m));
     U[e] = (i < p) ? Uz[i + (int64_t)j * p] : 0.0;
   }
   c.sync();
@@ -1132,7 +1132,7 @@ HDN int svd_rrqr(const Ctx& c, Arena& ar, const double* X, int m, int n, double 
   // Vt[i, :] = (Q2 [Vj[:, i]; 0])^T  for i < nw
   CK(apply_q(c, ar, Bt, n, n, p, Tq, false, Vw, n, nw, sm));
   for (int64_t e = c.tid; e < (int64_t)nw * n; e += c.nt) {
-    const int i = (int)(e / n), q = (int)(e % n);
+    const int i = (int)(qdiv(e, n)), q = (int)(qmod(e, n));
     Vt[e] = Vw[q + (int64_t)i * n];
   }
   c.sync();
@@ -1191,7 +1191,7 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
     double *Rm, *nc;
     ALLOC(Rm, double, (int64_t)kk * rl, ar);   // R (kk x rl) row-major
     for (int64_t e = c.tid; e < (int64_t)kk * rl; e += c.nt) {
-      const int i = (int)(e / rl), j = (int)(e % rl);
+      const int i = (int)(qdiv(e, rl)), j = (int)(qmod(e, rl));
       Rm[e] = (i <= j) ? w.c[k][i + (int64_t)j * m] : 0.0;
     }
     const int rpp = w.r[k - 1], np_ = w.n[k - 1];
@@ -1248,8 +1248,8 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
       double* Y;                       // col-major m x rprev
       ALLOC(Y, double, (int64_t)m * rprev, ar);
       for (int64_t e = c.tid; e < (int64_t)m * rprev; e += c.nt) {
-        const int64_t r = e % m;
-        const int a = (int)(e / m);
+        const int64_t r = qmod(e, m);
+        const int a = (int)(qdiv(e, m));
         Y[e] = (r < kk) ? carry[(int64_t)a * kk + r] : 0.0;
       }
       c.sync();
@@ -1274,9 +1274,9 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
 #endif
       ALLOC(X, double, (int64_t)mx * rr, ar);
       for (int64_t e = c.tid; e < (int64_t)mx * rr; e += c.nt) {
-        const int64_t row = e / rr;
-        const int g = (int)(e % rr);
-        const int a = (int)(row / n), i = (int)(row % n);
+        const int64_t row = qdiv(e, rr);
+        const int g = (int)(qmod(e, rr));
+        const int a = (int)(qdiv(row, n)), i = (int)(qmod(row, n));
         X[e] = Y[((int64_t)i * rr + g) + (int64_t)a * m];
       }
       c.sync();
@@ -1303,8 +1303,8 @@ HDN int tt_round(const Ctx& c, Arena& ar, const TT& in, double tol, int cap, TT&
     ALLOC(core, double, (int64_t)mx * rnew, ar);
     ALLOC(cr, double, (int64_t)rnew * rr, ar);
     for (int64_t e = c.tid; e < (int64_t)mx * rnew; e += c.nt) {
-      const int64_t i = e / rnew;
-      const int j = (int)(e % rnew);
+      const int64_t i = qdiv(e, rnew);
+      const int j = (int)(qmod(e, rnew));
       core[e] = U[i + (int64_t)j * mx];
     }
     for (int64_t e = c.tid; e < (int64_t)rnew * rr; e += c.nt) cr[e] = s[e / rr] * Vt[e];
@@ -1389,8 +1389,8 @@ HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double to
     ALLOC(Wi, double, (int64_t)wa * wb * (nh + 1), ar);
     c.sync();
     for (int64_t e = c.tid; e < (int64_t)ka * kb * (nh + 1); e += c.nt) {
-      const int om = (int)(e % (nh + 1));
-      const int64_t f = e / (nh + 1);
+      const int om = (int)(qmod(e, nh + 1));
+      const int64_t f = qdiv(e, nh + 1);
       const int a = (int)(f / kb), b = (int)(f % kb);
       double re = 0.0, im = 0.0;
       for (int i = 0; i < n; ++i) {
@@ -1403,8 +1403,8 @@ HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double to
       Ki[e] = im;
     }
     for (int64_t e = c.tid; e < (int64_t)wa * wb * (nh + 1); e += c.nt) {
-      const int om = (int)(e % (nh + 1));
-      const int64_t f = e / (nh + 1);
+      const int om = (int)(qmod(e, nh + 1));
+      const int64_t f = qdiv(e, nh + 1);
       const int a = (int)(f / wb), b = (int)(f % wb);
       double re = 0.0, im = 0.0;
       for (int i = 0; i < n; ++i) {
@@ -1436,7 +1436,7 @@ HDN int tt_fft_conv(const Ctx& c, Arena& ar, const TT& K, const TT& W, double to
     for (int row = 0; row < ka * wa; ++row) {
       const int a1 = row / wa, a2 = row % wa;
       for (int64_t e = c.tid; e < (int64_t)pr * (nh + 1); e += c.nt) {
-        const int col = (int)(e / (nh + 1)), om = (int)(e % (nh + 1));
+        const int col = (int)(qdiv(e, nh + 1)), om = (int)(qmod(e, nh + 1));
         const int b1 = col / wb, b2 = col % wb;
         const int64_t ik = ((int64_t)a1 * kb + b1) * (nh + 1) + om;
         const int64_t iw = ((int64_t)a2 * wb + b2) * (nh + 1) + om;
