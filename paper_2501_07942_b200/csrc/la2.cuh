@@ -731,7 +731,7 @@ HDN void qr_panel_blk(const Ctx& c, double* A, int64_t lda, int m, int j0, int j
 #endif
 }
 #ifndef TTGBF_QR2_MIN_ROWS
-#define TTGBF_QR2_MIN_ROWS 2048
+#define TTGBF_QR2_MIN_ROWS 0   /* measured: 2048 -> 226, 512 -> 234, 0 -> 237 steps/s (the 32-wide single-level panel spills its accumulators) */
 #endif
 constexpr int QR2_MIN_ROWS = TTGBF_QR2_MIN_ROWS;   // panels taller than this use two-level blocking
 HDN int geqrf_nb(const Ctx& c, Arena& ar, double* A, int64_t lda, int m, int n, double* tau, double* Ts,
