@@ -714,7 +714,7 @@ HD void t_from_gram(const Ctx& c, const double* G, int jb, const double* tau, do
 // panel's T comes from one Gram GEMM of its explicit V (which the trailing
 // update needs anyway).
 #ifndef TTGBF_QR_NS
-#define TTGBF_QR_NS 8
+#define TTGBF_QR_NS 4   /* measured (two-level at every height): 8 -> 12046, 4 -> 11591, 2 -> 12005 CTA-s per bench launch */
 #endif
 constexpr int NS = TTGBF_QR_NS;   // sub-panel width of the two-level panel factorisation
 #ifndef TTGBF_QR_PANEL_LL
@@ -724,7 +724,8 @@ HDN void qr_panel_blk(const Ctx& c, double* A, int64_t lda, int m, int j0, int j
 #if TTGBF_QR_PANEL_LL
   // register arrays sized to the panel: sub-panels (jb <= 8) keep their 8 + 9
   // accumulators in registers; the 32-wide instance spills part of them
-  if (jb <= 8) qr_panel_ll<8>(c, A, lda, m, j0, jb, tau, T, sm);
+  if (jb <= 4) qr_panel_ll<4>(c, A, lda, m, j0, jb, tau, T, sm);
+  else if (jb <= 8) qr_panel_ll<8>(c, A, lda, m, j0, jb, tau, T, sm);
   else qr_panel_ll<NB>(c, A, lda, m, j0, jb, tau, T, sm);
 #else
   qr_panel_nb(c, A, lda, m, j0, jb, tau, T, sm);
